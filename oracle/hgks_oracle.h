@@ -1,0 +1,127 @@
+/*
+ * hgks_oracle.h — plain CPU fp64 oracle for the HGKS S2O4 stage (arXiv 2207.01173 §2).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2207_01173_b200/, libhgks.so) never links, imports or executes it, and the two
+ * share no code, header, table or constant generator.
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; O-n / A.n = SURVEY.md §8(c)
+ * readings and Appendix A formula sheet (the readings are restated in DESIGN.md).
+ *
+ * Every function here is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
+ * against something other than itself (quadrature, closed forms, paper tables,
+ * invariants).  Pins are listed next to each declaration.
+ */
+#ifndef HGKS_ORACLE_H
+#define HGKS_ORACLE_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OR_NV 5      /* conservative variables (rho, rhoU, rhoV, rhoW, rhoE) */
+#define OR_NG 3      /* ghost layers (O-16) */
+#define OR_NM 9      /* velocity-moment tables hold orders 0..8 */
+
+/* gas + transport model (P:202-204 gamma/K; P:270-273 tau=mu/p; P:971-973 power law) */
+typedef struct {
+  double gamma;   /* specific heat ratio                                         */
+  double K;       /* internal DOF, or_K(gamma) (O-20)                      */
+  double prandtl; /* Pr; 1 = no heat-flux fix (TGV)                        */
+  int    mu_law;  /* 0: mu = mu_ref ; 1: mu = mu_ref*(T/T_ref)^omega, T = p/rho     */
+  double mu_ref, T_ref, omega;
+} or_gas;
+
+/* uniform-grid geometry of a block that carries OR_NG ghost layers on every side */
+typedef struct {
+  int    n[3];     /* interior cells nx, ny, nz                 */
+  double dx[3];    /* cell widths                               */
+  int    bc[3];    /* 0 periodic (only periodic is implemented) */
+} or_grid;
+
+double or_K(double gamma);
+
+/* A.2: normalised Maxwellian u-moments <u^n>, n = 0..OR_NM-1.
+ * which = 0 full space, +1 u>0 half space, -1 u<0 half space.
+ * Pin: scipy quadrature (test_oracle_kinetic.py::test_moments_vs_quadrature). */
+void or_moments_u(double U, double lam, int which, double m[OR_NM]);
+
+/* <u^a v^b w^c xi^(2d) psi> (5-vector) for a Maxwellian (rho-normalised), u-table chosen by
+ * which.  Pin: 5-D Gauss-Hermite quadrature. */
+void or_psi_moment(double U, double V, double W, double lam, double K, int which,
+                   int a, int b, int c, int d, double out[5]);
+
+/* conservative -> Maxwellian parameters (rho,U,V,W,lambda); A.1.  returns 0, or -1 if invalid */
+int or_cons_to_maxw(const double q[5], double K, double mx[5]);
+
+/* A.3 compatibility solve <(a.psi) psi>_g = b (rho-normalised), by assembling the 5x5 moment
+ * matrix from or_psi_moment and Gaussian elimination with partial pivoting.
+ * Pin: quadrature residual (test_slope_solve_residual). */
+int or_slope_solve(const double mx[5], double K, const double b[5], double a[5]);
+
+/* time integrals gamma_1..gamma_6 of the six time functions of Eq. (6) over [0,T]
+ * (A.6).  Pin: scipy.quad of the six kernels. */
+void or_time_integrals(double T, double tau, double g[6]);
+
+/* Gauss-point flux (A4-A6) in the local frame (u = face normal):
+ *   Wl, Wr         left/right conservative states at the Gauss point
+ *   dWl[i], dWr[i] their derivatives along local axis i (0 normal, 1 t1, 2 t2)
+ *   dW0[i]         equilibrium derivatives (O-6)
+ *   dt             step; the two windows are [0,dt/2] and [0,dt]
+ * Outputs F^n, dF = d_t F^n (Eq. (8) two-window solve), and tau.  Returns 0 or -1 on an
+ * invalid state.  Pins: Euler flux of a uniform state, Navier-Stokes limit (A.8),
+ * brute-force velocity-space quadrature of Eq. (6) (test_gp_flux_vs_quadrature). */
+int or_gp_flux(const or_gas* g, const double Wl[5], const double dWl[3][5],
+               const double Wr[5], const double dWr[3][5], const double dW0[3][5], double dt,
+               double F[5], double dF[5], double* tau);
+
+/* WENO5-Z (O-1, A.9) value at the right edge of the middle cell of q[0..4] = Qbar_{i-2..i+2}.
+ * Pins: constant/linear exactness, 5th-order convergence, linear-weight limit. */
+double or_weno5z_right(const double q[5]);
+double or_weno5z_left(const double q[5]);
+
+/* Gauss-point inputs of one face from a 6 (normal) x 5 (t1) x 5 (t2) block of cell averages
+ * cells[n][a][b] (n = i-2..i+3 normal, a = t1 offset -2..2, b = t2 offset -2..2), with cell
+ * widths h = (h_n, h_t1, h_t2).  For Gauss point gp = 2*m + n (m index in t1, n in t2, point
+ * -sqrt(3)/6 first), component c:
+ *   Wl[gp][c], Wr[gp][c], dWl[gp][i][c], dWr[gp][i][c], dW0[gp][i][c]   (i: normal, t1, t2)
+ * Steps A2-A3 with readings O-3, O-4, O-6.  Pins: trilinear exactness, constants. */
+void or_face_gauss_points(const double cells[6][5][5][5], const double h[3],
+                          double Wl[4][5], double Wr[4][5], double dWl[4][3][5],
+                          double dWr[4][3][5], double dW0[4][3][5]);
+
+/* Whole-grid periodic ghost fill of q laid out [5][nz+6][ny+6][nx+6] (O-16). */
+void or_fill_ghosts_periodic(const or_grid* gr, double* q);
+
+/* Operator L(Q) and d_t L(Q) (Eqs. (3)-(4)) on the interior of a ghosted
+ * block q [5][nz+6][ny+6][nx+6] whose ghosts are already filled.  L, dL are [5][nz][ny][nx].
+ * Returns 0, or -1 on an invalid Gauss-point state. */
+int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt,
+                double* L, double* dL);
+
+/* S2O4 stage updates (Eq. (7)) on flat arrays of length n:
+ *   stage 1: qs = q + dt/2 L + dt^2/8 dL
+ *   final  : qn = q + dt L + dt^2/6 (dL + 2 dLs)
+ * Pin: S:284 surrogate q' = q. */
+void or_s2o4_stage1(long n, const double* q, const double* L, const double* dL, double dt,
+                    double* qs);
+void or_s2o4_final(long n, const double* q, const double* L, const double* dL,
+                   const double* dLs, double dt, double* qn);
+
+/* CFL time step (O-13): dt = cfl * min over cells, d of dx_d/(|U_d| + c), c = sqrt(gamma p/rho),
+ * on an unghosted [5][nz][ny][nx] state.  Pin: Table 3. */
+double or_cfl_dt(const or_gas* g, const or_grid* gr, const double* q, double cfl);
+
+/* Full periodic S2O4 steps on an unghosted [5][nz][ny][nx] state, in place.
+ * dt_fixed > 0 uses it; else CFL each step.  dt_hist (nsteps, may be NULL) receives the dt
+ * used.  Returns 0, or -1 on an invalid state (q then holds the last good state). */
+int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed,
+           double cfl, double* dt_hist);
+
+/* Number of OpenMP threads the oracle uses (1 when built without OpenMP). */
+int or_num_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

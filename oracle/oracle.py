@@ -1,0 +1,225 @@
+"""ctypes wrapper of the plain CPU fp64 oracle (oracle/hgks_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, ``__graft_entry__.smoke()`` and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs may import this module.  The product path
+(``paper_2207_01173_b200``) never imports it; the two share no code.
+
+Arrays use the ABI layout [5][nz][ny][nx] (x fastest), float64, C-contiguous.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "liboracle.so")
+SRC = os.path.join(HERE, "hgks_oracle.c")
+
+_dp = C.POINTER(C.c_double)
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2, OpenMP, strict IEEE: no -ffast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
+        os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "hgks_oracle.h"))
+    ):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-fopenmp", "-fPIC", "-shared",
+             "-fno-fast-math", "-ffp-contract=off", "-o", LIB, SRC, "-lm"]
+        )
+    return LIB
+
+
+class Gas(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("K", C.c_double), ("prandtl", C.c_double),
+                ("mu_law", C.c_int), ("mu_ref", C.c_double), ("T_ref", C.c_double),
+                ("omega", C.c_double)]
+
+
+class Grid(C.Structure):
+    _fields_ = [("n", C.c_int * 3), ("dx", C.c_double * 3), ("bc", C.c_int * 3)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        L.or_K.restype = C.c_double
+        L.or_K.argtypes = [C.c_double]
+        L.or_moments_u.argtypes = [C.c_double, C.c_double, C.c_int, _dp]
+        L.or_psi_moment.argtypes = [C.c_double] * 5 + [C.c_int] * 5 + [_dp]
+        L.or_cons_to_maxw.argtypes = [_dp, C.c_double, _dp]
+        L.or_slope_solve.argtypes = [_dp, C.c_double, _dp, _dp]
+        L.or_time_integrals.argtypes = [C.c_double, C.c_double, _dp]
+        L.or_gp_flux.argtypes = [C.POINTER(Gas), _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp]
+        L.or_weno5z_right.restype = C.c_double
+        L.or_weno5z_right.argtypes = [_dp]
+        L.or_weno5z_left.restype = C.c_double
+        L.or_weno5z_left.argtypes = [_dp]
+        L.or_face_gauss_points.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.or_fill_ghosts_periodic.argtypes = [C.POINTER(Grid), _dp]
+        L.or_operator.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double, _dp, _dp]
+        L.or_s2o4_stage1.argtypes = [C.c_long, _dp, _dp, _dp, C.c_double, _dp]
+        L.or_s2o4_final.argtypes = [C.c_long, _dp, _dp, _dp, _dp, C.c_double, _dp]
+        L.or_cfl_dt.restype = C.c_double
+        L.or_cfl_dt.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double]
+        L.or_run.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_int, C.c_double,
+                             C.c_double, _dp]
+        L.or_num_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def _arr(x, shape=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def K_of(gamma: float) -> float:
+    return lib().or_K(gamma)
+
+
+def make_gas(gamma=1.4, mu=0.0, prandtl=1.0, mu_law=0, T_ref=1.0, omega=0.0) -> Gas:
+    return Gas(gamma, K_of(gamma), prandtl, mu_law, mu, T_ref, omega)
+
+
+def make_grid(n, dx) -> Grid:
+    g = Grid()
+    for d in range(3):
+        g.n[d] = int(n[d])
+        g.dx[d] = float(dx[d])
+        g.bc[d] = 0
+    return g
+
+
+def moments_u(U, lam, which):
+    m = np.zeros(9)
+    lib().or_moments_u(U, lam, which, _p(m))
+    return m
+
+
+def psi_moment(U, V, W, lam, K, which, a, b, c, d):
+    out = np.zeros(5)
+    lib().or_psi_moment(U, V, W, lam, K, which, a, b, c, d, _p(out))
+    return out
+
+
+def cons_to_maxw(q, K):
+    q = _arr(q)
+    mx = np.zeros(5)
+    rc = lib().or_cons_to_maxw(_p(q), K, _p(mx))
+    return None if rc else mx
+
+
+def slope_solve(mx, K, b):
+    mx, b = _arr(mx), _arr(b)
+    a = np.zeros(5)
+    assert lib().or_slope_solve(_p(mx), K, _p(b), _p(a)) == 0
+    return a
+
+
+def time_integrals(T, tau):
+    g = np.zeros(6)
+    lib().or_time_integrals(T, tau, _p(g))
+    return g
+
+
+def gp_flux(gas: Gas, Wl, dWl, Wr, dWr, dW0, dt):
+    Wl, Wr = _arr(Wl, (5,)), _arr(Wr, (5,))
+    dWl, dWr, dW0 = _arr(dWl, (3, 5)), _arr(dWr, (3, 5)), _arr(dW0, (3, 5))
+    F, dF, tau = np.zeros(5), np.zeros(5), np.zeros(1)
+    rc = lib().or_gp_flux(C.byref(gas), _p(Wl), _p(dWl), _p(Wr), _p(dWr), _p(dW0), dt, _p(F),
+                          _p(dF), _p(tau))
+    if rc:
+        raise ValueError("invalid Gauss-point state")
+    return F, dF, float(tau[0])
+
+
+def weno5z(q, side="right"):
+    q = _arr(q, (5,))
+    f = lib().or_weno5z_right if side == "right" else lib().or_weno5z_left
+    return f(_p(q))
+
+
+def face_gauss_points(cells, h):
+    """cells: [6 normal][5 t1][5 t2][5 comp] -> dict of GP inputs."""
+    cells, h = _arr(cells, (6, 5, 5, 5)), _arr(h, (3,))
+    Wl, Wr = np.zeros((4, 5)), np.zeros((4, 5))
+    dWl, dWr, dW0 = np.zeros((4, 3, 5)), np.zeros((4, 3, 5)), np.zeros((4, 3, 5))
+    lib().or_face_gauss_points(_p(cells), _p(h), _p(Wl), _p(Wr), _p(dWl), _p(dWr), _p(dW0))
+    return dict(Wl=Wl, Wr=Wr, dWl=dWl, dWr=dWr, dW0=dW0)
+
+
+def ghosted(q: np.ndarray, ng: int = 3) -> np.ndarray:
+    """[5][nz][ny][nx] -> [5][nz+6][ny+6][nx+6] with periodic ghosts filled by the oracle."""
+    q = _arr(q)
+    _, nz, ny, nx = q.shape
+    qg = np.zeros((5, nz + 2 * ng, ny + 2 * ng, nx + 2 * ng))
+    qg[:, ng:-ng, ng:-ng, ng:-ng] = q
+    lib().or_fill_ghosts_periodic(C.byref(make_grid((nx, ny, nz), (1, 1, 1))), _p(qg))
+    return qg
+
+
+def operator(gas: Gas, q: np.ndarray, dx, dt: float, qg: np.ndarray | None = None):
+    """L(Q), d_t L(Q) for a periodic state (or a pre-ghosted block qg)."""
+    q = _arr(q)
+    _, nz, ny, nx = q.shape
+    if qg is None:
+        qg = ghosted(q)
+    qg = _arr(qg)
+    L, dL = np.zeros_like(q), np.zeros_like(q)
+    rc = lib().or_operator(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(qg), dt, _p(L),
+                           _p(dL))
+    if rc:
+        raise ValueError("invalid state inside operator")
+    return L, dL
+
+
+def s2o4_stage1(q, L, dL, dt):
+    q, L, dL = _arr(q), _arr(L), _arr(dL)
+    qs = np.zeros_like(q)
+    lib().or_s2o4_stage1(q.size, _p(q), _p(L), _p(dL), dt, _p(qs))
+    return qs
+
+
+def s2o4_final(q, L, dL, dLs, dt):
+    q, L, dL, dLs = _arr(q), _arr(L), _arr(dL), _arr(dLs)
+    qn = np.zeros_like(q)
+    lib().or_s2o4_final(q.size, _p(q), _p(L), _p(dL), _p(dLs), dt, _p(qn))
+    return qn
+
+
+def cfl_dt(gas: Gas, q: np.ndarray, dx, cfl: float = 0.4) -> float:
+    q = _arr(q)
+    _, nz, ny, nx = q.shape
+    return lib().or_cfl_dt(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(q), cfl)
+
+
+def run(gas: Gas, q: np.ndarray, dx, nsteps: int, dt_fixed: float = 0.0, cfl: float = 0.4):
+    """Advance a periodic state nsteps full S2O4 steps; returns (q_new, dt_history)."""
+    q = _arr(q).copy()
+    _, nz, ny, nx = q.shape
+    hist = np.zeros(max(nsteps, 1))
+    rc = lib().or_run(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(q), nsteps, dt_fixed,
+                      cfl, _p(hist))
+    if rc:
+        raise ValueError("oracle run hit an invalid state")
+    return q, hist[:nsteps]
+
+
+def num_threads() -> int:
+    return lib().or_num_threads()
