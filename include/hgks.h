@@ -1,0 +1,142 @@
+/*
+ * hgks.h — C ABI of the B200-native HGKS S2O4 step library (libhgks.so).
+ *
+ * Method: one full two-stage fourth-order (S2O4) step of the high-order gas-kinetic scheme of
+ * arXiv 2207.01173 §2 on a structured 3D grid of cell-averaged conservative variables
+ *   Q = (rho, rhoU, rhoV, rhoW, rhoE)
+ * advanced by Eq. (7)
+ *   Q*      = Q^n + dt/2 L(Q^n) + dt^2/8 d_t L(Q^n)
+ *   Q^{n+1} = Q^n + dt L(Q^n) + dt^2/6 (d_t L(Q^n) + 2 d_t L(Q*))
+ * with L = -(1/|Omega|) sum_faces F (Eqs. (3)-(4)), face fluxes from 2x2 Gauss points
+ * of the BGK time-dependent distribution Eq. (6), linearised in time by
+ * the two-window solve Eq. (8), fifth-order WENO reconstruction, and the
+ * CFL time step of Alg. 1.  The readings of every point the paper leaves open are
+ * listed in DESIGN.md ("Readings"), numbered as in SURVEY.md §8(c) (O-1 .. O-26).
+ *
+ * Conventions
+ *   - Every call is collective over the nranks of one context (same order on every rank).
+ *   - Return codes: HGKS_OK (0) or a negative hgks_status; a message is kept per context
+ *     (hgks_last_error(ctx)) or per thread when ctx is NULL.
+ *   - The ABI is always fp64 and uses the layout [5][nz_local][ny][nx] (x fastest, variable
+ *     outermost) for states; fp32 contexts round on set_state and widen on get_state.
+ *   - The library owns all device memory, its streams (unless one is passed in) and the NCCL
+ *     communicator; callers own every pointer they pass and keep ownership after the call.
+ *   - There is no CPU fallback: every compute step runs in sm_100a kernels; without a usable
+ *     CUDA device hgks_create fails with HGKS_ECUDA.
+ */
+#ifndef HGKS_H
+#define HGKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hgks_ctx hgks_ctx; /* opaque: device buffers, streams, NCCL comm, status */
+
+typedef enum {
+  HGKS_OK = 0,
+  HGKS_EINVAL = -1, /* bad argument / parameter combination                                  */
+  HGKS_ECUDA = -2,  /* CUDA runtime error (context must then be destroyed)                     */
+  HGKS_ENCCL = -3,  /* NCCL error (context must then be destroyed)                             */
+  HGKS_ESTATE = -4, /* rho<=0, p<=0 or non-finite state; first bad global cell in last_error  */
+  HGKS_ENOMEM = -5  /* device allocation failed                                                */
+} hgks_status;
+
+typedef enum { HGKS_FP64 = 0, HGKS_FP32 = 1 } hgks_precision;      /* P:1091-1093 FP32/FP64 builds */
+typedef enum { HGKS_PERIODIC = 0, HGKS_WALL_ISOTHERMAL = 1 } hgks_bc;
+typedef enum { HGKS_MU_CONST = 0, HGKS_MU_POWER = 1 } hgks_mu_law;
+
+typedef struct {
+  int32_t n[3];          /* GLOBAL interior cells (nx, ny, nz); each >= 5; nz/nranks >= 3           */
+  double lo[3], hi[3];   /* box: uniform spacing dx_d = (hi_d - lo_d)/n_d                           */
+  hgks_bc bc[3];         /* per axis (both ends); only HGKS_PERIODIC is accepted in this build      */
+  double gamma;          /* 1 < gamma <= 5/3 ; K = (5 - 3 gamma)/(gamma - 1)              */
+  double prandtl;        /* Pr; only Pr == 1 is accepted in this build                     */
+  hgks_mu_law mu_law;    /* mu = mu_ref (const) or mu_ref (T/T_ref)^omega with T = p/rho          */
+  double mu_ref, T_ref, omega;
+  double cfl;            /* > 0: adaptive dt = cfl / max_cells max_d (|U_d| + c)/dx_d (O-13)       */
+  double dt_fixed;       /* > 0: fixed dt, overrides cfl (parity / timing runs)                    */
+  hgks_precision precision;
+  int32_t rank, nranks;  /* slab decomposition along z (outermost storage axis)                   */
+  int32_t device;        /* CUDA device ordinal used by this context                              */
+  const void* nccl_id;   /* 128-byte ncclUniqueId identical on all ranks; NULL iff nranks == 1     */
+  void* stream;          /* cudaStream_t for all work; NULL => the library creates one            */
+} hgks_params;
+
+/* Validate p, allocate device memory, create streams and (nranks > 1) the NCCL communicator.
+ * *out receives the context, or NULL on failure.  Errors: EINVAL, ECUDA, ENCCL, ENOMEM. */
+int hgks_create(const hgks_params* p, hgks_ctx** out);
+
+/* This rank's slab: global z planes [z_begin, z_begin + nz_local).  Planes are split as evenly as
+ * possible, lower ranks taking the remainder (see hgks_slab_of). */
+int hgks_local_extent(const hgks_ctx* c, int32_t* z_begin, int32_t* nz_local);
+
+/* Copy in this rank's slab q[5][nz_local][ny][nx] (fp64; host pointer, or device pointer when
+ * on_device != 0), check validity (rho > 0, p > 0, finite; HGKS_ESTATE names the first bad
+ * global cell) and, in CFL mode, compute the first step's global max wave speed.  q is not
+ * retained. */
+int hgks_set_state(hgks_ctx* c, const double* q, int on_device);
+
+/* Advance up to nsteps S2O4 steps.  dt per step is dt_fixed, or the CFL value from
+ * the global max wave speed (one 8-byte NCCL max-allreduce per step).  If t_end > 0 the last dt
+ * is clamped so t does not pass t_end and the call stops there.  *t_inout is read (start time)
+ * and written (time reached); *dt_last (may be NULL) receives the last dt taken.  All steps are
+ * enqueued without host round trips; the call reads one status word at the end.
+ * On HGKS_ESTATE the state is rolled back to the last good Q^n and *t_inout is that step's start
+ * time. */
+int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double* dt_last);
+
+/* Copy out this rank's slab in the set_state layout (fp64; host or device pointer). Synchronises. */
+int hgks_get_state(hgks_ctx* c, double* q, int on_device);
+
+/* Release everything owned by c.  NULL-safe. */
+int hgks_destroy(hgks_ctx* c);
+
+/* Last error message of c (or of the calling thread when c == NULL); never NULL. */
+const char* hgks_last_error(const hgks_ctx* c);
+
+/* ---- small helpers (host logic, no device work) ----------------------------------------- */
+
+/* Size of the opaque NCCL unique id (128) and generator for rank 0 (broadcast it yourself). */
+size_t hgks_nccl_id_bytes(void);
+int hgks_get_nccl_id(void* out);
+
+/* Slab of `rank` among `nranks` for nz planes: [*z_begin, *z_begin + *nz_local). */
+int hgks_slab_of(int32_t nz, int32_t rank, int32_t nranks, int32_t* z_begin, int32_t* nz_local);
+
+/* Halo plan of the z decomposition (periodic ring): neighbours, and the element offsets (in the
+ * ghosted fp32/fp64 device layout [nz_local+6][5][ny+6][nx+6]) of the 3-plane chunks sent to and
+ * received from each neighbour.  count = elements per chunk.  Used by hgks_step's NCCL exchange
+ * and exported so the host logic can be exercised without a GPU. */
+typedef struct {
+  int32_t up, down;                 /* neighbour ranks (rank+1, rank-1 mod nranks)          */
+  int64_t send_up, recv_down;       /* top interior planes -> up ; bottom ghosts <- down    */
+  int64_t send_down, recv_up;       /* bottom interior planes -> down ; top ghosts <- up    */
+  int64_t count;                    /* elements in one 3-plane chunk                        */
+} hgks_halo_plan;
+int hgks_make_halo_plan(int32_t nx, int32_t ny, int32_t nz_local, int32_t rank, int32_t nranks,
+                        hgks_halo_plan* out);
+
+/* ---- instrumentation (bench.py roofline / launch accounting) ----------------------------- */
+
+/* Kernel classes timed with CUDA events when profiling is enabled. */
+typedef enum {
+  HGKS_K_FLUX_X = 0, HGKS_K_FLUX_Y = 1, HGKS_K_FLUX_Z = 2, HGKS_K_UPDATE = 3,
+  HGKS_K_GHOST = 4, HGKS_K_HALO = 5, HGKS_K_DT = 6, HGKS_K_COUNT = 7
+} hgks_kernel_class;
+
+/* enable != 0: bracket every launch of each class with CUDA events on the compute stream.
+ * Resets the accumulators. */
+int hgks_profile_enable(hgks_ctx* c, int enable);
+/* Synchronise and read: ms[k] = summed event time of class k, launches[k] = launches of class k
+ * since the last enable/reset; total_launches = all kernels this library launched since then. */
+int hgks_profile_read(hgks_ctx* c, double ms[HGKS_K_COUNT], int64_t launches[HGKS_K_COUNT],
+                      int64_t* total_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGKS_H */

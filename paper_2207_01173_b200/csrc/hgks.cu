@@ -1,0 +1,611 @@
+// hgks.cu — C ABI (include/hgks.h, include/hgks_test.h) and host runtime of libhgks.so.
+//
+// Owns: device state buffers (double-buffered Q^n / R, Q*), the three face-flux arrays, the
+// control block, the compute stream, the NCCL communicator (slab halos along z + the 8-byte
+// max-allreduce of the CFL wave speed), and launch/timing instrumentation.
+// Every compute step is a kernel from hgks_kernels.cuh; there is no host or CPU fallback.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "../../include/hgks.h"
+#include "../../include/hgks_test.h"
+#include "hgks_kernels.cuh"
+
+using namespace hgks;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct Prof {
+  bool on = false;
+  bool created = false;
+  cudaEvent_t ev[2 * 4096] = {};
+  int nev = 0;
+  int cls[4096];
+  double ms[HGKS_K_COUNT] = {0};
+  long long launches[HGKS_K_COUNT] = {0};
+};
+
+}  // namespace
+
+struct hgks_ctx {
+  hgks_params p{};
+  int n[3] = {0, 0, 0};  // global
+  int nzl = 0, z0 = 0;
+  double h[3] = {0, 0, 0};
+  bool fp32 = false;
+  size_t esz = 8;
+  size_t qelems = 0;     // elements of one ghosted state
+  size_t nface[3] = {0, 0, 0};
+  void* Q[2] = {nullptr, nullptr};
+  void* Qs = nullptr;
+  void* F[3] = {nullptr, nullptr, nullptr};
+  double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
+  Ctl* ctl = nullptr;
+  Ctl* ctl_host = nullptr;    // pinned
+  int cur = 0;
+  bool have_state = false;
+  cudaStream_t s = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  hgks_halo_plan plan{};
+  int dev = 0;
+  long long total_launches = 0;
+  Prof prof;
+  std::string err;
+};
+
+static int fail(hgks_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_thread_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(c, call)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail((c), HGKS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define NCCL_TRY(c, call)                                                                   \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess) return fail((c), HGKS_ENCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+// ---- instrumentation ------------------------------------------------------------------------
+static void prof_begin(hgks_ctx* c, int cls) {
+  c->prof.launches[cls] += 1;
+  if (!c->prof.on || c->prof.nev >= 4096) return;
+  int k = c->prof.nev;
+  c->prof.cls[k] = cls;
+  cudaEventRecord(c->prof.ev[2 * k], c->s);
+}
+static void prof_end(hgks_ctx* c, int cls) {
+  (void)cls;
+  if (!c->prof.on || c->prof.nev >= 4096) return;
+  cudaEventRecord(c->prof.ev[2 * c->prof.nev + 1], c->s);
+  c->prof.nev += 1;
+}
+static void prof_flush(hgks_ctx* c) {  // fold recorded events into ms[] (caller synchronised)
+  for (int k = 0; k < c->prof.nev; ++k) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->prof.ev[2 * k], c->prof.ev[2 * k + 1]) == cudaSuccess) c->prof.ms[c->prof.cls[k]] += ms;
+  }
+  c->prof.nev = 0;
+}
+
+template <typename T>
+static Geo<T> make_geo(const hgks_ctx* c) {
+  Geo<T> g;
+  g.n[0] = c->n[0];
+  g.n[1] = c->n[1];
+  g.n[2] = c->nzl;
+  g.px = c->n[0] + 6;
+  g.py = c->n[1] + 6;
+  g.vs = (long long)g.py * g.px;
+  g.plane = 5 * g.vs;
+  for (int d = 0; d < 3; ++d) {
+    g.h[d] = T(c->h[d]);
+    g.ih[d] = T(1.0 / c->h[d]);
+  }
+  g.z0 = c->z0;
+  g.nx_g = c->n[0];
+  g.ny_g = c->n[1];
+  return g;
+}
+
+template <typename T>
+static GasK<T> make_gas(const hgks_params& p) {
+  GasK<T> g;
+  g.K = T((5.0 - 3.0 * p.gamma) / (p.gamma - 1.0));  // P:202, evaluated in fp64 (O-20)
+  g.gamma = T(p.gamma);
+  g.mu_ref = T(p.mu_ref);
+  g.T_ref = T(p.T_ref > 0 ? p.T_ref : 1.0);
+  g.omega = T(p.omega);
+  g.mu_law = (int)p.mu_law;
+  return g;
+}
+
+static int blocks_for(long long n, int tpb) { return (int)std::min<long long>((n + tpb - 1) / tpb, 148LL * 64); }
+
+// ---- ghost layers: x/y periodic kernel, then z by local copy (1 rank) or NCCL (slab halo) ----
+template <typename T>
+static int fill_ghosts(hgks_ctx* c, T* q) {
+  Geo<T> g = make_geo<T>(c);
+  long long total = (long long)g.n[2] * g.plane;
+  prof_begin(c, HGKS_K_GHOST);
+  ghost_xy_kernel<T><<<blocks_for(total, 256), 256, 0, c->s>>>(q, g, c->ctl);
+  prof_end(c, HGKS_K_GHOST);
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  const hgks_halo_plan& pl = c->plan;
+  prof_begin(c, HGKS_K_HALO);
+  if (c->p.nranks == 1) {
+    size_t bytes = (size_t)pl.count * sizeof(T);
+    CUDA_TRY(c, cudaMemcpyAsync(q + pl.recv_down, q + pl.send_up, bytes, cudaMemcpyDeviceToDevice, c->s));
+    CUDA_TRY(c, cudaMemcpyAsync(q + pl.recv_up, q + pl.send_down, bytes, cudaMemcpyDeviceToDevice, c->s));
+  } else {
+    ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    NCCL_TRY(c, ncclGroupStart());
+    NCCL_TRY(c, ncclSend(q + pl.send_up, pl.count, ty, pl.up, c->comm, c->s));
+    NCCL_TRY(c, ncclRecv(q + pl.recv_down, pl.count, ty, pl.down, c->comm, c->s));
+    NCCL_TRY(c, ncclSend(q + pl.send_down, pl.count, ty, pl.down, c->comm, c->s));
+    NCCL_TRY(c, ncclRecv(q + pl.recv_up, pl.count, ty, pl.up, c->comm, c->s));
+    NCCL_TRY(c, ncclGroupEnd());
+  }
+  prof_end(c, HGKS_K_HALO);
+  return HGKS_OK;
+}
+
+template <typename T, int STAGE>
+static int flux_sweeps(hgks_ctx* c, const T* q) {
+  Geo<T> g = make_geo<T>(c);
+  GasK<T> gas = make_gas<T>(c->p);
+  const size_t smem = flux_smem_bytes<T>();
+  static bool attr_done[2][2] = {{false, false}, {false, false}};
+  const int pi = sizeof(T) == 8 ? 0 : 1;
+  if (!attr_done[pi][STAGE - 1]) {
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done[pi][STAGE - 1] = true;
+  }
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  {  // x faces: t1 = y, t2 = z
+    dim3 grid((ny + TT1 - 1) / TT1, (nz + TT2 - 1) / TT2, nx + 1);
+    prof_begin(c, HGKS_K_FLUX_X);
+    flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[0], g, gas, c->ctl);
+    prof_end(c, HGKS_K_FLUX_X);
+  }
+  {  // y faces: t1 = z, t2 = x
+    dim3 grid((nz + TT1 - 1) / TT1, (nx + TT2 - 1) / TT2, ny + 1);
+    prof_begin(c, HGKS_K_FLUX_Y);
+    flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[1], g, gas, c->ctl);
+    prof_end(c, HGKS_K_FLUX_Y);
+  }
+  {  // z faces: t1 = x, t2 = y
+    dim3 grid((nx + TT1 - 1) / TT1, (ny + TT2 - 1) / TT2, nz + 1);
+    prof_begin(c, HGKS_K_FLUX_Z);
+    flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[2], g, gas, c->ctl);
+    prof_end(c, HGKS_K_FLUX_Z);
+  }
+  c->total_launches += 3;
+  CUDA_TRY(c, cudaGetLastError());
+  return HGKS_OK;
+}
+
+template <typename T>
+static int run_steps(hgks_ctx* c, int nsteps) {
+  Geo<T> g = make_geo<T>(c);
+  const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
+  const int tpb = 256;
+  const int ublocks = (int)((ncell + tpb - 1) / tpb);
+  int rc;
+  for (int s = 0; s < nsteps; ++s) {
+    T* Qn = (T*)c->Q[c->cur];
+    T* R = (T*)c->Q[c->cur ^ 1];
+    T* Qs = (T*)c->Qs;
+    prof_begin(c, HGKS_K_DT);
+    dt_kernel<<<1, 32, 0, c->s>>>(c->ctl);
+    prof_end(c, HGKS_K_DT);
+    c->total_launches += 1;
+    // stage 1 at Q^n
+    if ((rc = fill_ghosts<T>(c, Qn))) return rc;
+    if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
+    prof_begin(c, HGKS_K_UPDATE);
+    update_kernel<T, 1><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, c->p.gamma, c->ctl);
+    prof_end(c, HGKS_K_UPDATE);
+    // stage 2 at Q* (same dt and windows, O-11)
+    if ((rc = fill_ghosts<T>(c, Qs))) return rc;
+    if ((rc = flux_sweeps<T, 2>(c, Qs))) return rc;
+    prof_begin(c, HGKS_K_UPDATE);
+    update_kernel<T, 2><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, c->p.gamma, c->ctl);
+    prof_end(c, HGKS_K_UPDATE);
+    c->total_launches += 2;
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->p.nranks > 1) {  // global max wave speed + global error flag
+      NCCL_TRY(c, ncclAllReduce(&c->ctl->red[0], &c->ctl->red[0], 2, ncclUint64, ncclMax, c->comm, c->s));
+    }
+    c->cur ^= 1;
+  }
+  commit_kernel<<<1, 32, 0, c->s>>>(c->ctl);
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  return HGKS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* hgks_last_error(const hgks_ctx* c) { return c ? c->err.c_str() : g_thread_err.c_str(); }
+
+size_t hgks_nccl_id_bytes(void) { return sizeof(ncclUniqueId); }
+
+int hgks_get_nccl_id(void* out) {
+  if (!out) return fail(nullptr, HGKS_EINVAL, "hgks_get_nccl_id: out is NULL");
+  ncclUniqueId id;
+  NCCL_TRY(nullptr, ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return HGKS_OK;
+}
+
+int hgks_slab_of(int32_t nz, int32_t rank, int32_t nranks, int32_t* z_begin, int32_t* nz_local) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || nz < nranks || !z_begin || !nz_local)
+    return fail(nullptr, HGKS_EINVAL, "hgks_slab_of: bad arguments (nz=%d rank=%d nranks=%d)", nz, rank, nranks);
+  int base = nz / nranks, rem = nz % nranks;
+  *nz_local = base + (rank < rem ? 1 : 0);
+  *z_begin = rank * base + (rank < rem ? rank : rem);
+  return HGKS_OK;
+}
+
+int hgks_make_halo_plan(int32_t nx, int32_t ny, int32_t nz_local, int32_t rank, int32_t nranks, hgks_halo_plan* out) {
+  if (!out || nx < 1 || ny < 1 || nz_local < 3 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(nullptr, HGKS_EINVAL, "hgks_make_halo_plan: bad arguments");
+  const int64_t plane = 5LL * (ny + 6) * (nx + 6);  // one ghosted z plane (all 5 variables)
+  out->up = (rank + 1) % nranks;
+  out->down = (rank + nranks - 1) % nranks;
+  out->count = 3 * plane;
+  out->send_up = (int64_t)nz_local * plane;         // interior planes nz_l-3..nz_l-1 (ghosted z = nz_l..nz_l+2)
+  out->recv_down = 0;                               // ghost planes -3..-1
+  out->send_down = 3 * plane;                       // interior planes 0..2
+  out->recv_up = (int64_t)(nz_local + 3) * plane;   // ghost planes nz_l..nz_l+2
+  return HGKS_OK;
+}
+
+int hgks_create(const hgks_params* p, hgks_ctx** out) {
+  if (!out) return fail(nullptr, HGKS_EINVAL, "hgks_create: out is NULL");
+  *out = nullptr;
+  if (!p) return fail(nullptr, HGKS_EINVAL, "hgks_create: params is NULL");
+  for (int d = 0; d < 3; ++d) {
+    if (p->n[d] < 5) return fail(nullptr, HGKS_EINVAL, "n[%d]=%d < 5", d, p->n[d]);
+    if (!(p->hi[d] > p->lo[d])) return fail(nullptr, HGKS_EINVAL, "hi[%d] <= lo[%d]", d, d);
+    if (p->bc[d] != HGKS_PERIODIC) return fail(nullptr, HGKS_EINVAL, "only periodic boundaries are implemented");
+  }
+  if (!(p->gamma > 1.0 && p->gamma <= 5.0 / 3.0 + 1e-12)) return fail(nullptr, HGKS_EINVAL, "gamma=%g outside (1, 5/3]", p->gamma);
+  if (p->prandtl != 1.0) return fail(nullptr, HGKS_EINVAL, "prandtl=%g: only Pr = 1 is implemented", p->prandtl);
+  if (!(p->mu_ref >= 0.0)) return fail(nullptr, HGKS_EINVAL, "mu_ref < 0");
+  if (p->mu_law == HGKS_MU_POWER && !(p->T_ref > 0.0)) return fail(nullptr, HGKS_EINVAL, "T_ref must be > 0 for the power law");
+  if (!(p->dt_fixed > 0.0) && !(p->cfl > 0.0)) return fail(nullptr, HGKS_EINVAL, "need cfl > 0 or dt_fixed > 0");
+  if (p->precision != HGKS_FP64 && p->precision != HGKS_FP32) return fail(nullptr, HGKS_EINVAL, "bad precision");
+  if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(nullptr, HGKS_EINVAL, "bad rank/nranks");
+  if (p->nranks > 1 && !p->nccl_id) return fail(nullptr, HGKS_EINVAL, "nranks > 1 needs nccl_id");
+  if (p->n[2] / p->nranks < 3) return fail(nullptr, HGKS_EINVAL, "nz/nranks < 3");
+
+  hgks_ctx* c = new hgks_ctx();
+  c->p = *p;
+  c->p.nccl_id = nullptr;
+  for (int d = 0; d < 3; ++d) {
+    c->n[d] = p->n[d];
+    c->h[d] = (p->hi[d] - p->lo[d]) / p->n[d];
+  }
+  hgks_slab_of(p->n[2], p->rank, p->nranks, &c->z0, &c->nzl);
+  c->fp32 = p->precision == HGKS_FP32;
+  c->esz = c->fp32 ? 4 : 8;
+  c->dev = p->device;
+  auto bail = [&](int code) {
+    std::string e = c->err;
+    hgks_destroy(c);
+    g_thread_err = e;
+    return code;
+  };
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete c;
+    return fail(nullptr, HGKS_ECUDA, "no CUDA device available (libhgks has no CPU fallback)");
+  }
+  if (cudaSetDevice(c->dev) != cudaSuccess) {
+    fail(c, HGKS_ECUDA, "cudaSetDevice(%d) failed", c->dev);
+    return bail(HGKS_ECUDA);
+  }
+  if (p->stream) {
+    c->s = (cudaStream_t)p->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) != cudaSuccess) {
+      fail(c, HGKS_ECUDA, "stream creation failed");
+      return bail(HGKS_ECUDA);
+    }
+    c->own_stream = true;
+  }
+  hgks_make_halo_plan(c->n[0], c->n[1], c->nzl, p->rank, p->nranks, &c->plan);
+  c->qelems = (size_t)(c->nzl + 6) * 5 * (c->n[1] + 6) * (c->n[0] + 6);
+  c->nface[0] = (size_t)(c->n[0] + 1) * c->n[1] * c->nzl;
+  c->nface[1] = (size_t)c->n[0] * (c->n[1] + 1) * c->nzl;
+  c->nface[2] = (size_t)c->n[0] * c->n[1] * (c->nzl + 1);
+  bool ok = true;
+  for (int b = 0; b < 2; ++b) ok = ok && cudaMalloc(&c->Q[b], c->qelems * c->esz) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->Qs, c->qelems * c->esz) == cudaSuccess;
+  for (int d = 0; d < 3; ++d) ok = ok && cudaMalloc(&c->F[d], 10 * c->nface[d] * c->esz) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->stage64, 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double)) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->ctl, sizeof(Ctl)) == cudaSuccess;
+  ok = ok && cudaMallocHost(&c->ctl_host, sizeof(Ctl)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    fail(c, HGKS_ENOMEM, "device allocation failed");
+    return bail(HGKS_ENOMEM);
+  }
+  // zero ghosts once (they are always overwritten before use) and the face arrays
+  for (int b = 0; b < 2; ++b) cudaMemsetAsync(c->Q[b], 0, c->qelems * c->esz, c->s);
+  cudaMemsetAsync(c->Qs, 0, c->qelems * c->esz, c->s);
+  Ctl h{};
+  h.t = 0;
+  h.dt_fixed = p->dt_fixed;
+  h.cfl = p->cfl;
+  h.bad_cell = ~0ull;
+  *c->ctl_host = h;
+  if (cudaMemcpyAsync(c->ctl, c->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, c->s) != cudaSuccess ||
+      cudaStreamSynchronize(c->s) != cudaSuccess) {
+    fail(c, HGKS_ECUDA, "initialisation copy failed");
+    return bail(HGKS_ECUDA);
+  }
+  if (p->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, p->nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&c->comm, p->nranks, id, p->rank);
+    if (r != ncclSuccess) {
+      fail(c, HGKS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      c->comm = nullptr;
+      return bail(HGKS_ENCCL);
+    }
+  }
+  *out = c;
+  return HGKS_OK;
+}
+
+int hgks_local_extent(const hgks_ctx* c, int32_t* z_begin, int32_t* nz_local) {
+  if (!c || !z_begin || !nz_local) return fail(nullptr, HGKS_EINVAL, "hgks_local_extent: NULL argument");
+  *z_begin = c->z0;
+  *nz_local = c->nzl;
+  return HGKS_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+static int set_state_t(hgks_ctx* c) {
+  Geo<T> g = make_geo<T>(c);
+  const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
+  T* Q = (T*)c->Q[c->cur];
+  pack_kernel<T><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>(c->stage64, Q, g);
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  h->red[0] = 0;
+  h->red[1] = 0;
+  h->bad_cell = ~0ull;
+  h->halt = 0;
+  h->pending = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
+  cfl_kernel<T><<<blocks_for(ncell, 256), 256, 0, c->s>>>(Q, g, c->p.gamma, c->ctl);
+  c->total_launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  if (c->p.nranks > 1)
+    NCCL_TRY(c, ncclAllReduce(&c->ctl->red[0], &c->ctl->red[0], 2, ncclUint64, ncclMax, c->comm, c->s));
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  if (h->red[1]) {
+    if (h->bad_cell != ~0ull) {
+      unsigned long long b = h->bad_cell;
+      long long i = b % c->n[0], j = (b / c->n[0]) % c->n[1], k = b / ((unsigned long long)c->n[0] * c->n[1]);
+      return fail(c, HGKS_ESTATE, "invalid state (rho<=0, p<=0 or non-finite) at global cell (i,j,k)=(%lld,%lld,%lld)", i, j, k);
+    }
+    return fail(c, HGKS_ESTATE, "invalid state on another rank");
+  }
+  h->smax_cur = h->red[0];
+  h->red[0] = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  c->have_state = true;
+  return HGKS_OK;
+}
+
+extern "C" {
+
+int hgks_set_state(hgks_ctx* c, const double* q, int on_device) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_set_state: ctx is NULL");
+  if (!q) return fail(c, HGKS_EINVAL, "hgks_set_state: q is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
+  CUDA_TRY(c, cudaMemcpyAsync(c->stage64, q, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
+  return c->fp32 ? set_state_t<float>(c) : set_state_t<double>(c);
+}
+
+int hgks_get_state(hgks_ctx* c, double* q, int on_device) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_get_state: ctx is NULL");
+  if (!q) return fail(c, HGKS_EINVAL, "hgks_get_state: q is NULL");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_get_state: no state set");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  const long long ncell = (long long)c->n[0] * c->n[1] * c->nzl;
+  if (c->fp32) unpack_kernel<float><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>((const float*)c->Q[c->cur], c->stage64, make_geo<float>(c));
+  else unpack_kernel<double><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>((const double*)c->Q[c->cur], c->stage64, make_geo<double>(c));
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(q, c->stage64, 5 * ncell * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  return HGKS_OK;
+}
+
+int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double* dt_last) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_step: ctx is NULL");
+  if (!t_inout) return fail(c, HGKS_EINVAL, "hgks_step: t_inout is NULL");
+  if (nsteps < 0) return fail(c, HGKS_EINVAL, "hgks_step: nsteps < 0");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_step: call hgks_set_state first");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  // reset per-call control: t, t_end, counters (one small H2D copy)
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  h->t = *t_inout;
+  h->t_end = t_end;
+  h->halt = 0;
+  h->pending = 0;
+  h->steps_done = 0;
+  h->bad_cell = ~0ull;
+  CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
+  const int cur0 = c->cur;
+  int rc = c->fp32 ? run_steps<float>(c, nsteps) : run_steps<double>(c, nsteps);
+  if (rc) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  c->cur = cur0 ^ (int)(h->steps_done & 1);  // buffer holding the last committed state
+  *t_inout = h->t;
+  if (dt_last) *dt_last = h->dt_last;
+  if (h->halt == 1) {
+    if (h->bad_cell != ~0ull) {
+      unsigned long long b = h->bad_cell;
+      long long i = b % c->n[0], j = (b / c->n[0]) % c->n[1], k = b / ((unsigned long long)c->n[0] * c->n[1]);
+      return fail(c, HGKS_ESTATE, "invalid state after step %lld at global cell (i,j,k)=(%lld,%lld,%lld); rolled back",
+                  h->steps_done, i, j, k);
+    }
+    return fail(c, HGKS_ESTATE, "invalid state after step %lld on another rank; rolled back", h->steps_done);
+  }
+  return HGKS_OK;
+}
+
+int hgks_destroy(hgks_ctx* c) {
+  if (!c) return HGKS_OK;
+  cudaSetDevice(c->dev);
+  if (c->s) cudaStreamSynchronize(c->s);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (int b = 0; b < 2; ++b) cudaFree(c->Q[b]);
+  cudaFree(c->Qs);
+  for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
+  cudaFree(c->stage64);
+  cudaFree(c->ctl);
+  if (c->ctl_host) cudaFreeHost(c->ctl_host);
+  for (int k = 0; k < 2 * 4096; ++k)
+    if (c->prof.ev[k]) cudaEventDestroy(c->prof.ev[k]);
+  if (c->own_stream && c->s) cudaStreamDestroy(c->s);
+  delete c;
+  return HGKS_OK;
+}
+
+int hgks_profile_enable(hgks_ctx* c, int enable) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_profile_enable: ctx is NULL");
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  if (enable && !c->prof.created) {
+    for (int k = 0; k < 2 * 4096; ++k) CUDA_TRY(c, cudaEventCreate(&c->prof.ev[k]));
+    c->prof.created = true;
+  }
+  c->prof.on = enable != 0;
+  c->prof.nev = 0;
+  for (int k = 0; k < HGKS_K_COUNT; ++k) {
+    c->prof.ms[k] = 0;
+    c->prof.launches[k] = 0;
+  }
+  c->total_launches = 0;
+  return HGKS_OK;
+}
+
+int hgks_profile_read(hgks_ctx* c, double ms[HGKS_K_COUNT], int64_t launches[HGKS_K_COUNT], int64_t* total_launches) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_profile_read: ctx is NULL");
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  prof_flush(c);
+  for (int k = 0; k < HGKS_K_COUNT; ++k) {
+    if (ms) ms[k] = c->prof.ms[k];
+    if (launches) launches[k] = c->prof.launches[k];
+  }
+  if (total_launches) *total_launches = c->total_launches;
+  return HGKS_OK;
+}
+
+// ---- test entry points (include/hgks_test.h) --------------------------------------------------
+int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, double T_ref, double omega, double dt,
+                      const double* in, int64_t n, double* out) {
+  if (!in || !out || n < 0) return fail(nullptr, HGKS_EINVAL, "hgks_test_gp_flux: bad arguments");
+  if (n == 0) return HGKS_OK;
+  hgks_params p{};
+  p.gamma = gamma;
+  p.mu_law = (hgks_mu_law)mu_law;
+  p.mu_ref = mu_ref;
+  p.T_ref = T_ref;
+  p.omega = omega;
+  double *din = nullptr, *dout = nullptr;
+  CUDA_TRY(nullptr, cudaMalloc(&din, 55 * n * sizeof(double)));
+  CUDA_TRY(nullptr, cudaMalloc(&dout, 11 * n * sizeof(double)));
+  CUDA_TRY(nullptr, cudaMemcpy(din, in, 55 * n * sizeof(double), cudaMemcpyHostToDevice));
+  int blocks = (int)((n + 127) / 128);
+  if (precision == HGKS_FP32) gp_flux_test_kernel<float><<<blocks, 128>>>(din, dout, n, make_gas<float>(p), (float)dt);
+  else gp_flux_test_kernel<double><<<blocks, 128>>>(din, dout, n, make_gas<double>(p), dt);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, 11 * n * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(din);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(nullptr, HGKS_ECUDA, "hgks_test_gp_flux: %s", cudaGetErrorString(e));
+  return HGKS_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
+  Geo<T> g = make_geo<T>(c);
+  T* Q = (T*)c->Q[c->cur];
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  h->dt = dt;
+  h->halt = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
+  int rc;
+  if ((rc = fill_ghosts<T>(c, Q))) return rc;
+  if ((rc = flux_sweeps<T, 1>(c, Q))) return rc;
+  const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
+  double *dL_ = nullptr, *dDL = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dL_, 5 * ncell * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&dDL, 5 * ncell * sizeof(double)));
+  operator_out_kernel<T><<<(int)((ncell + 255) / 256), 256, 0, c->s>>>((T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dL_, dDL);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(L, dL_, 5 * ncell * sizeof(double), cudaMemcpyDeviceToHost, c->s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dL, dDL, 5 * ncell * sizeof(double), cudaMemcpyDeviceToHost, c->s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->s);
+  cudaFree(dL_);
+  cudaFree(dDL);
+  if (e != cudaSuccess) return fail(c, HGKS_ECUDA, "hgks_test_operator: %s", cudaGetErrorString(e));
+  return HGKS_OK;
+}
+
+extern "C" {
+
+int hgks_test_operator(hgks_ctx* c, double dt, double* L, double* dL) {
+  if (!c || !L || !dL || !(dt > 0)) return fail(c, HGKS_EINVAL, "hgks_test_operator: bad arguments");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_test_operator: no state");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  return c->fp32 ? test_operator_t<float>(c, dt, L, dL) : test_operator_t<double>(c, dt, L, dL);
+}
+
+}  // extern "C"

@@ -1,0 +1,426 @@
+// hgks_kernels.cuh — sm_100a kernels of one S2O4 stage (product path).
+//
+//   flux_kernel<T, DIR, STAGE>  fused: normal WENO reconstruction of a tile of face lines into
+//                               shared memory (A2) -> tangential pass t1 (A3) -> per-Gauss-point
+//                               thread: tangential pass t2 + BGK flux (A4-A6) -> 4-point face
+//                               quadrature by warp shuffles (A7) -> face-flux array
+//   update_kernel<T, STAGE>     flux divergence L, d_t L (Eqs. (3)-(4)) + Eq. (7) stage update,
+//                               stage-2 epilogue: validity flags + CFL wave-speed max (A0, A8)
+//   ghost_xy_kernel<T>          periodic ghost layers along x and y (A1, O-16)
+//   cfl_kernel<T> / dt_kernel   initial wave-speed max, per-step dt + commit logic (A0)
+//
+// Layout of a ghosted state (elements of T): [nz_l+6][5][ny+6][nx+6], x fastest.
+// A face-flux array of direction d: [10][fz][fy][fx] with f_a = n_a + (a == d); components
+// 0..4 = F^n, 5..9 = d_t F^n (per unit face area, i.e. 1/4 sum over the 2x2 Gauss points).
+#pragma once
+#include "gks_device.cuh"
+
+namespace hgks {
+
+// device control block (one per context)
+struct Ctl {
+  double t, dt, dt_last;
+  double t_end;                 // <= 0: none
+  double dt_fixed, cfl;
+  unsigned long long smax_cur;  // bits of the max wave speed of the current state
+  unsigned long long red[2];    // [0] smax of the newest state, [1] error flag (allreduced, max)
+  unsigned long long bad_cell;  // min linear global index of an invalid cell (ULLONG_MAX: none)
+  int halt;                     // 0 running, 1 invalid state, 2 reached t_end
+  int pending;                  // 1: a step has run and awaits commit
+  long long steps_done;         // committed steps in the current hgks_step call
+};
+
+template <typename T>
+struct Geo {
+  int n[3];        // local interior cells (nx, ny, nz_local)
+  int px, py;      // pitches: nx+6, ny+6
+  long long plane; // 5*py*px: stride of one z plane
+  long long vs;    // py*px: stride of one variable
+  T h[3];          // cell widths
+  T ih[3];         // 1/h
+  int z0;          // global z of local plane 0
+  int ny_g, nx_g;  // global sizes (for linear cell ids)
+};
+
+template <typename T>
+__device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, int k) {
+  return (long long)(k + 3) * g.plane + (long long)v * g.vs + (long long)(j + 3) * g.px + (i + 3);
+}
+
+constexpr int TT1 = 8, TT2 = 8;            // faces per tile along t1, t2
+constexpr int TL1 = TT1 + 4, TL2 = TT2 + 4;  // lines per tile (+-2 tangential halo)
+constexpr int NTHREADS_FLUX = TT1 * TT2 * 4;
+constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
+
+template <typename T>
+constexpr size_t flux_smem_bytes() {
+  return sizeof(T) * (6 * 5 * TL2 * TL1 + TT1 * TL2 * 2 * 5 * NB);
+}
+
+template <typename T, int DIR, int STAGE>
+__global__ void __launch_bounds__(NTHREADS_FLUX, 1)
+    flux_kernel(const T* __restrict__ q, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sA = reinterpret_cast<T*>(smem_raw);     // [6][5][TL2][TL1]
+  T* sB = sA + 6 * 5 * TL2 * TL1;             // [TT1][TL2][2][5][NB]
+
+  const int nN = g.n[DIR], n1 = g.n[A1], n2 = g.n[A2];
+  const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2, fn = blockIdx.z;  // face fn: cells fn-1 | fn
+  const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
+  const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
+  const long long s2 = (A2 == 0) ? 1 : (A2 == 1 ? g.px : g.plane);
+  const T ihN = g.ih[DIR];
+  (void)nN;
+
+  // ---- phase A: normal reconstruction of TL1 x TL2 lines, 5 components --------------------
+  for (int w = threadIdx.x; w < TL1 * TL2 * 5; w += NTHREADS_FLUX) {
+    const int l1 = w % TL1;
+    const int rest = w / TL1;
+    const int l2 = rest % TL2;
+    const int c = rest / TL2;
+    int g1 = t10 + l1 - 2, g2 = t20 + l2 - 2;
+    g1 = min(max(g1, -3), n1 + 2);  // ragged tiles: clamp (values unused)
+    g2 = min(max(g2, -3), n2 + 2);
+    const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 1 + DIR : (c == 2 ? 1 + A1 : 1 + A2)));
+    // cell (fn - 3) along the normal, (g1, g2) tangentially; interior index origin at +3 ghosts
+    long long base = 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs + (long long)(fn - 3) * sN + g1 * s1 + g2 * s2;
+    T s[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) s[r] = q[base + r * sN];
+    T f[6];
+    normal_fields(s, ihN, f);
+#pragma unroll
+    for (int ff = 0; ff < 6; ++ff) sA[((ff * 5 + c) * TL2 + l2) * TL1 + l1] = f[ff];
+  }
+  __syncthreads();
+
+  // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
+  for (int w = threadIdx.x; w < TT1 * TL2 * 2 * 5; w += NTHREADS_FLUX) {
+    const int c = w % 5;
+    int rest = w / 5;
+    const int m = rest % 2;
+    rest /= 2;
+    const int l2 = rest % TL2;
+    const int a = rest / TL2;
+    T out[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) out[k] = T(0);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const T wv = T(kWV[m][r]), wd = T(kWD[m][r]);
+#pragma unroll
+      for (int ff = 0; ff < 6; ++ff) {
+        const T x = sA[((ff * 5 + c) * TL2 + l2) * TL1 + a + r];
+        out[ff] += wv * x;
+        if (ff == 0) out[6] += wd * x;
+        if (ff == 1) out[7] += wd * x;
+        if (ff == 4) out[8] += wd * x;
+      }
+    }
+    T* dst = sB + ((((a * TL2 + l2) * 2 + m) * 5 + c) * NB);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) dst[k] = out[k];
+  }
+  __syncthreads();
+
+  // ---- phase C: one thread per Gauss point --------------------------------------------------
+  const int gp = threadIdx.x & 3, face = threadIdx.x >> 2;
+  const int m = gp >> 1, nn = gp & 1;
+  const int a = face % TT1, b = face / TT1;
+  const T ih1 = g.ih[A1], ih2 = g.ih[A2];
+  T Wl[5], Wr[5], dWl[3][5], dWr[3][5], dW0[3][5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    T v[NB];
+    T d2[3];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) v[k] = T(0);
+    d2[0] = d2[1] = d2[2] = T(0);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const T wv = T(kWV[nn][r]), wd = T(kWD[nn][r]);
+      const T* src = sB + ((((a * TL2 + b + r) * 2 + m) * 5 + c) * NB);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) v[k] += wv * src[k];
+      d2[0] += wd * src[0];
+      d2[1] += wd * src[1];
+      d2[2] += wd * src[4];
+    }
+    Wl[c] = v[0];
+    Wr[c] = v[1];
+    dWl[0][c] = v[2];
+    dWr[0][c] = v[3];
+    dW0[0][c] = v[5];
+    dWl[1][c] = v[6] * ih1;
+    dWr[1][c] = v[7] * ih1;
+    dW0[1][c] = v[8] * ih1;
+    dWl[2][c] = d2[0] * ih2;
+    dWr[2][c] = d2[1] * ih2;
+    dW0[2][c] = d2[2] * ih2;
+  }
+  T F[5], dF[5], tau;
+  gp_flux<T, STAGE == 1>(gas, Wl, Wr, dWl, dWr, dW0, T(ctl->dt), F, dF, tau);
+  // 2x2 Gauss quadrature, omega_mn = 1/4 (O-8): lanes 4f..4f+3 hold the face's Gauss points
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    if (STAGE == 1) {
+      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 1);
+      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 2);
+    }
+    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 1);
+    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 2);
+  }
+  const int f1 = t10 + a, f2 = t20 + b;
+  if (gp == 0 && f1 < n1 && f2 < n2) {
+    int cd[3];
+    cd[DIR] = fn;
+    cd[A1] = f1;
+    cd[A2] = f2;
+    const int fx = g.n[0] + (DIR == 0), fy = g.n[1] + (DIR == 1), fz = g.n[2] + (DIR == 2);
+    const long long nface = (long long)fx * fy * fz;
+    const long long id = ((long long)cd[2] * fy + cd[1]) * fx + cd[0];
+    const int gc[5] = {0, 1 + DIR, 1 + A1, 1 + A2, 4};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (STAGE == 1) flux[gc[k] * nface + id] = T(0.25) * F[k];
+      flux[(5 + gc[k]) * nface + id] = T(0.25) * dF[k];
+    }
+  }
+}
+
+// ---- periodic ghosts along x and y over the interior z planes (A1; O-16) ----------------------
+template <typename T>
+__global__ void ghost_xy_kernel(T* __restrict__ q, Geo<T> g, const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  const long long total = (long long)g.n[2] * 5 * (g.py) * (g.px);
+  const int nx = g.n[0], ny = g.n[1];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int ii = (int)(e % g.px);
+    long long r = e / g.px;
+    const int jj = (int)(r % g.py);
+    r /= g.py;
+    const int v = (int)(r % 5);
+    const int k = (int)(r / 5);
+    const int i = ii - 3, j = jj - 3;
+    if (i >= 0 && i < nx && j >= 0 && j < ny) continue;
+    const int si = (i + nx) % nx, sj = (j + ny) % ny;  // n >= 5 > 3: one wrap suffices
+    q[qidx(g, v, i, j, k)] = q[qidx(g, v, si, sj, k)];
+  }
+}
+
+// max over d of (|U_d| + c)/dx_d for one cell (O-13); c = sqrt(gamma p / rho)
+template <typename T>
+__device__ __forceinline__ double wave_speed(const T (&c5)[5], const Geo<T>& g, double gamma, bool& ok) {
+  double rho = (double)c5[0];
+  double U = (double)c5[1] / rho, V = (double)c5[2] / rho, W = (double)c5[3] / rho;
+  double p = (gamma - 1.0) * ((double)c5[4] - 0.5 * rho * (U * U + V * V + W * W));
+  ok = (rho > 0.0) && (p > 0.0) && isfinite(rho) && isfinite(p) && isfinite(U) && isfinite(V) && isfinite(W);
+  double c = sqrt(gamma * p / rho);
+  double sx = (fabs(U) + c) * (double)g.ih[0], sy = (fabs(V) + c) * (double)g.ih[1], sz = (fabs(W) + c) * (double)g.ih[2];
+  return fmax(sx, fmax(sy, sz));
+}
+
+__device__ __forceinline__ void block_max_commit(double s, unsigned long long* dst) {
+  // warp max, then one atomic per warp (atomicMax on the bit pattern orders non-negative doubles)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0 && s > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(s));
+}
+
+// ---- flux divergence + S2O4 stage update (Eqs. (3)-(4), (7)) ----------------------------------
+// STAGE 1: Qs = Q + dt/2 L + dt^2/8 dL ;  R = Q + dt L + dt^2/6 dL
+// STAGE 2: R  = R + dt^2/3 dL(Q*)  (= Q^{n+1}); epilogue: validity + wave speed into ctl->red
+template <typename T, int STAGE>
+__global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
+                              const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
+                              Geo<T> g, double gamma, Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const long long ncell = (long long)nx * ny * nz;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const double dt = ctl->dt;
+  double smax = 0.0;
+  if (e < ncell) {
+    const int i = (int)(e % nx);
+    const int j = (int)((e / nx) % ny);
+    const int k = (int)(e / ((long long)nx * ny));
+    const long long nfx = (long long)(nx + 1) * ny * nz, nfy = (long long)nx * (ny + 1) * nz, nfz = (long long)nx * ny * (nz + 1);
+    const long long ix = ((long long)k * ny + j) * (nx + 1) + i;
+    const long long iy = ((long long)k * (ny + 1) + j) * nx + i;
+    const long long iz = ((long long)k * ny + j) * nx + i;
+    const long long oy = nx, oz = (long long)nx * ny;
+    const T ihx = g.ih[0], ihy = g.ih[1], ihz = g.ih[2];
+    const T tdt = T(dt);
+    T out[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      const T dL = -((FX[(5 + c) * nfx + ix + 1] - FX[(5 + c) * nfx + ix]) * ihx +
+                     (FY[(5 + c) * nfy + iy + oy] - FY[(5 + c) * nfy + iy]) * ihy +
+                     (FZ[(5 + c) * nfz + iz + oz] - FZ[(5 + c) * nfz + iz]) * ihz);
+      const long long qi = qidx(g, c, i, j, k);
+      if (STAGE == 1) {
+        const T L = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * ihx + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * ihy +
+                      (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * ihz);
+        const T q = Q[qi];
+        Qs[qi] = q + T(0.5) * tdt * L + T(0.125) * tdt * tdt * dL;
+        R[qi] = q + tdt * L + (T(1) / T(6)) * tdt * tdt * dL;
+      } else {
+        const T v = R[qi] + (T(1) / T(3)) * tdt * tdt * dL;
+        R[qi] = v;
+        out[c] = v;
+      }
+    }
+    if (STAGE == 2) {
+      bool ok;
+      smax = wave_speed(out, g, gamma, ok);
+      if (!ok) {
+        smax = 0.0;
+        unsigned long long gid = ((unsigned long long)(k + g.z0) * g.ny_g + j) * g.nx_g + i;
+        atomicMin(&ctl->bad_cell, gid);
+        ctl->red[1] = 1ull;  // benign race: every writer stores 1
+      }
+    }
+  }
+  if (STAGE == 2) block_max_commit(smax, &ctl->red[0]);
+}
+
+// ---- wave-speed max / validity of the current state (set_state) ------------------------------
+template <typename T>
+__global__ void cfl_kernel(const T* __restrict__ Q, Geo<T> g, double gamma, Ctl* __restrict__ ctl) {
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const long long ncell = (long long)nx * ny * nz;
+  double smax = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ncell + 0; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
+    T c5[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) c5[c] = Q[qidx(g, c, i, j, k)];
+    bool ok;
+    double s = wave_speed(c5, g, gamma, ok);
+    if (!ok) {
+      unsigned long long gid = ((unsigned long long)(k + g.z0) * g.ny_g + j) * g.nx_g + i;
+      atomicMin(&ctl->bad_cell, gid);
+      ctl->red[1] = 1ull;
+    } else {
+      smax = fmax(smax, s);
+    }
+  }
+  block_max_commit(smax, &ctl->red[0]);
+}
+
+// ---- per-step control (A0): commit the previous step, then choose dt ------------------------
+__device__ __forceinline__ void commit_pending(Ctl* c) {
+  if (!c->pending) return;
+  c->pending = 0;
+  if (c->red[1]) {  // the step produced an invalid state somewhere (global after allreduce)
+    c->halt = 1;
+    return;
+  }
+  c->t += c->dt;
+  c->dt_last = c->dt;
+  c->steps_done += 1;
+  c->smax_cur = c->red[0];
+}
+
+__global__ void dt_kernel(Ctl* c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (c->halt) return;
+  commit_pending(c);
+  if (c->halt) return;
+  double dt = c->dt_fixed > 0.0 ? c->dt_fixed : c->cfl / __longlong_as_double((long long)c->smax_cur);
+  if (c->t_end > 0.0) {
+    double rem = c->t_end - c->t;
+    if (rem <= 1e-14 * c->t_end) {
+      c->halt = 2;
+      return;
+    }
+    if (dt > rem) dt = rem;
+  }
+  c->dt = dt;
+  c->red[0] = 0ull;
+  c->red[1] = 0ull;
+  c->pending = 1;
+}
+
+__global__ void commit_kernel(Ctl* c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (c->halt) return;
+  commit_pending(c);
+}
+
+// ---- layout conversion: ABI [5][nz][ny][nx] fp64 <-> ghosted [nz+6][5][ny+6][nx+6] T ----------
+template <typename T>
+__global__ void pack_kernel(const double* __restrict__ in, T* __restrict__ Q, Geo<T> g) {
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const long long ncell = (long long)nx * ny * nz;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 5 * ncell; e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e % ncell;
+    const int v = (int)(e / ncell);
+    const int i = (int)(s % nx), j = (int)((s / nx) % ny), k = (int)(s / ((long long)nx * ny));
+    Q[qidx(g, v, i, j, k)] = T(in[e]);
+  }
+}
+
+template <typename T>
+__global__ void unpack_kernel(const T* __restrict__ Q, double* __restrict__ out, Geo<T> g) {
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const long long ncell = (long long)nx * ny * nz;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 5 * ncell; e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e % ncell;
+    const int v = (int)(e / ncell);
+    const int i = (int)(s % nx), j = (int)((s / nx) % ny), k = (int)(s / ((long long)nx * ny));
+    out[e] = (double)Q[qidx(g, v, i, j, k)];
+  }
+}
+
+// L and d_t L from the face arrays (test entry hgks_test_operator), ABI layout, fp64
+template <typename T>
+__global__ void operator_out_kernel(const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
+                                    Geo<T> g, double* __restrict__ L, double* __restrict__ dL) {
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const long long ncell = (long long)nx * ny * nz;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= ncell) return;
+  const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
+  const long long nfx = (long long)(nx + 1) * ny * nz, nfy = (long long)nx * (ny + 1) * nz, nfz = (long long)nx * ny * (nz + 1);
+  const long long ix = ((long long)k * ny + j) * (nx + 1) + i;
+  const long long iy = ((long long)k * (ny + 1) + j) * nx + i;
+  const long long iz = ((long long)k * ny + j) * nx + i;
+  const long long oy = nx, oz = (long long)nx * ny;
+  for (int c = 0; c < 10; ++c) {
+    const T v = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * g.ih[0] + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * g.ih[1] +
+                  (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * g.ih[2]);
+    if (c < 5) L[c * ncell + e] = (double)v;
+    else dL[(c - 5) * ncell + e] = (double)v;
+  }
+}
+
+// batched Gauss-point flux (test entry hgks_test_gp_flux)
+template <typename T>
+__global__ void gp_flux_test_kernel(const double* __restrict__ in, double* __restrict__ out, long long n, GasK<T> gas, T dt) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double* r = in + 55 * e;
+  T Wl[5], Wr[5], dWl[3][5], dWr[3][5], dW0[3][5];
+  for (int k = 0; k < 5; ++k) {
+    Wl[k] = T(r[k]);
+    Wr[k] = T(r[5 + k]);
+    for (int i = 0; i < 3; ++i) {
+      dWl[i][k] = T(r[10 + 5 * i + k]);
+      dWr[i][k] = T(r[25 + 5 * i + k]);
+      dW0[i][k] = T(r[40 + 5 * i + k]);
+    }
+  }
+  T F[5], dF[5], tau;
+  gp_flux<T, true>(gas, Wl, Wr, dWl, dWr, dW0, dt, F, dF, tau);
+  double* o = out + 11 * e;
+  for (int k = 0; k < 5; ++k) {
+    o[k] = (double)F[k];
+    o[5 + k] = (double)dF[k];
+  }
+  o[10] = (double)tau;
+}
+
+}  // namespace hgks
