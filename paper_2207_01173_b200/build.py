@@ -29,19 +29,21 @@ def sources():
                   + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
     srcs = sources()
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
-        return LIB
+    out = out or LIB
+    if not force and os.path.exists(out) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
+        return out
     inc, nccl_so, nccl_dir = _nccl_dirs()
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", INCLUDE, "-I", inc, "-o", LIB, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
+           *["-D" + d for d in defines], "-I", INCLUDE, "-I", inc, "-o", out, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
            "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir]
     subprocess.check_call(cmd)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[5:] for a in sys.argv[1:] if a.startswith("-out=")]
+    print(build(force=True, verbose="-v" in sys.argv, out=outs[0] if outs else None, defines=defs))

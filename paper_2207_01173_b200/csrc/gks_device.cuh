@@ -23,16 +23,16 @@ namespace hgks {
 // ---------------------------------------------------------------------------------------------
 // precision-generic math
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ double m_sqrt(double x) { return sqrt(x); }
-__device__ __forceinline__ float m_sqrt(float x) { return sqrtf(x); }
-__device__ __forceinline__ double m_exp(double x) { return exp(x); }
-__device__ __forceinline__ float m_exp(float x) { return expf(x); }
-__device__ __forceinline__ double m_erfc(double x) { return erfc(x); }
-__device__ __forceinline__ float m_erfc(float x) { return erfcf(x); }
-__device__ __forceinline__ double m_pow(double x, double y) { return pow(x, y); }
-__device__ __forceinline__ float m_pow(float x, float y) { return powf(x, y); }
-__device__ __forceinline__ double m_abs(double x) { return fabs(x); }
-__device__ __forceinline__ float m_abs(float x) { return fabsf(x); }
+__host__ __device__ __forceinline__ double m_sqrt(double x) { return sqrt(x); }
+__host__ __device__ __forceinline__ float m_sqrt(float x) { return sqrtf(x); }
+__host__ __device__ __forceinline__ double m_exp(double x) { return exp(x); }
+__host__ __device__ __forceinline__ float m_exp(float x) { return expf(x); }
+__host__ __device__ __forceinline__ double m_erfc(double x) { return erfc(x); }
+__host__ __device__ __forceinline__ float m_erfc(float x) { return erfcf(x); }
+__host__ __device__ __forceinline__ double m_pow(double x, double y) { return pow(x, y); }
+__host__ __device__ __forceinline__ float m_pow(float x, float y) { return powf(x, y); }
+__host__ __device__ __forceinline__ double m_abs(double x) { return fabs(x); }
+__host__ __device__ __forceinline__ float m_abs(float x) { return fabsf(x); }
 
 template <typename T>
 struct GasK {
@@ -98,208 +98,337 @@ __device__ __forceinline__ void normal_fields(const T (&s)[6], T inv_h, T (&f)[6
 // -+sqrt(3)/6 (O-8), from the 5 face-averaged values j-2..j+2 (sympy-derived):
 // value weights WV[m][r], derivative weights WD[m][r] (per unit cell width).
 #define HGKS_S3 1.7320508075688772935274463415059
-__device__ __constant__ static const double kWV[2][5] = {
-    {-7.0 * HGKS_S3 / 432.0 - 1.0 / 4320.0, 1.0 / 1080.0 + 25.0 * HGKS_S3 / 216.0, 719.0 / 720.0,
-     1.0 / 1080.0 - 25.0 * HGKS_S3 / 216.0, -1.0 / 4320.0 + 7.0 * HGKS_S3 / 432.0},
-    {-1.0 / 4320.0 + 7.0 * HGKS_S3 / 432.0, 1.0 / 1080.0 - 25.0 * HGKS_S3 / 216.0, 719.0 / 720.0,
-     1.0 / 1080.0 + 25.0 * HGKS_S3 / 216.0, -7.0 * HGKS_S3 / 432.0 - 1.0 / 4320.0}};
-__device__ __constant__ static const double kWD[2][5] = {
-    {HGKS_S3 / 54.0 + 1.0 / 12.0, -2.0 / 3.0 - 13.0 * HGKS_S3 / 54.0, 4.0 * HGKS_S3 / 9.0,
-     2.0 / 3.0 - 13.0 * HGKS_S3 / 54.0, -1.0 / 12.0 + HGKS_S3 / 54.0},
-    {1.0 / 12.0 - HGKS_S3 / 54.0, -2.0 / 3.0 + 13.0 * HGKS_S3 / 54.0, -4.0 * HGKS_S3 / 9.0,
-     2.0 / 3.0 + 13.0 * HGKS_S3 / 54.0, -1.0 / 12.0 - HGKS_S3 / 54.0}};
+// point -sqrt(3)/6 (m = 0); the point +sqrt(3)/6 uses the mirror image (see the kernels)
+__host__ __device__ constexpr double kWV0(int r) {
+  return r == 0 ? -7.0 * HGKS_S3 / 432.0 - 1.0 / 4320.0
+       : r == 1 ? 1.0 / 1080.0 + 25.0 * HGKS_S3 / 216.0
+       : r == 2 ? 719.0 / 720.0
+       : r == 3 ? 1.0 / 1080.0 - 25.0 * HGKS_S3 / 216.0
+                : -1.0 / 4320.0 + 7.0 * HGKS_S3 / 432.0;
+}
+__host__ __device__ constexpr double kWD0(int r) {
+  return r == 0 ? HGKS_S3 / 54.0 + 1.0 / 12.0
+       : r == 1 ? -2.0 / 3.0 - 13.0 * HGKS_S3 / 54.0
+       : r == 2 ? 4.0 * HGKS_S3 / 9.0
+       : r == 3 ? 2.0 / 3.0 - 13.0 * HGKS_S3 / 54.0
+                : -1.0 / 12.0 + HGKS_S3 / 54.0;
+}
 
 // ---------------------------------------------------------------------------------------------
-// Kinetic part.  Moments <u^a v^b w^c (alpha.psi) psi> of one Maxwellian, with
-// psi = (1, u, v, w, (u^2+v^2+w^2+xi^2)/2).  Tables: u[0..6], v[0..5], w[0..5],
-// x1 = <xi^2>, x2 = <xi^4>.  All indices are compile-time so the tables stay in registers.
+// Kinetic part (A4-A6).  Every Maxwellian is handled in a frame moving with it, where its
+// velocity moments are those of an isotropic Gaussian (odd moments vanish), so each moment
+// vector <u^a v^b w^c (alpha.psi) psi> collapses to a handful of terms; results are
+// mapped back with the Galilean shift of psi = (1, u, v, w, (|u|^2 + xi^2)/2):
+//   psi_lab = T(s) psi_frame,   T(s) x = (x1, x2 + s_u x1, x3 + s_v x1, x4 + s_w x1,
+//                                          x5 + s.x_{2..4} + |s|^2 x1 / 2).
+// theta = 1/(2 lambda) is the temperature; <c^2> = theta, <c^4> = 3 theta^2, <xi^2> = K theta,
+// <xi^4> = K(K+2) theta^2.  g0 uses the fully co-moving frame; g_l / g_r (half spaces in u) use
+// the frame moving with their tangential velocity only, with the half-space u-moments t_n.
+// Identities used (derived in DESIGN.md "Kinetic algebra"; every one is exercised by the parity
+// tests against the oracle's generic moment code):
+//   compatibility inverse (isotropic):  a2..4 = b2..4/theta,  a5 = 2(b5 - (K+3)theta b1/2)/((K+3)theta^2),
+//                                      a1 = b1 - (K+3)theta a5/2
+//   Q_i(a) = <c_i (a.psi) psi> = theta a_{i+1} e_1 + theta(a1 + (K+5)theta a5/2) e_{i+1}
+//            + (K+5)theta^2 a_{i+1}/2 e_5
 // ---------------------------------------------------------------------------------------------
+#define HD __host__ __device__ __forceinline__
+
+// x <- T(su, sv, sw) x
 template <typename T>
-struct Tab {
-  T u[7], v[6], w[6];
-  T x1, x2;
+HD void shift_vec(T su, T sv, T sw, T (&x)[5]) {
+  const T x1 = x[0];
+  x[4] += su * x[1] + sv * x[2] + sw * x[3] + T(0.5) * (su * su + sv * sv + sw * sw) * x1;
+  x[1] += su * x1;
+  x[2] += sv * x1;
+  x[3] += sw * x1;
+}
+
+// One direction of the compatibility solves of one Maxwellian in its fully co-moving
+// frame: from the conservative derivative dW along local axis I, the spatial slope a_I
+// (<a_I> = dW_I / rho, O-7) and the contribution s_I b_c + Q_I(a_I) to
+// R = sum_i <u_i a_i.psi psi> (frame components), whose negative is M A.
+template <int I, typename T>
+HD void slope_dir(T K, T irho, T U, T V, T W, T th, T it, const T (&dW)[5], T (&a)[5], T (&R)[5]) {
+  const T hK3 = T(0.5) * (K + T(3)) * th;
+  const T c5 = T(2) / ((K + T(3)) * th * th);
+  const T hK5t = T(0.5) * (K + T(5)) * th;
+  const T b1 = dW[0] * irho, b2 = dW[1] * irho, b3 = dW[2] * irho, b4 = dW[3] * irho, b5 = dW[4] * irho;
+  // b_c = T(-s) b
+  const T c5v = b5 - U * b2 - V * b3 - W * b4 + T(0.5) * (U * U + V * V + W * W) * b1;
+  const T c2 = b2 - U * b1, c3 = b3 - V * b1, c4 = b4 - W * b1;
+  const T a5 = c5 * (c5v - hK3 * b1);
+  a[0] = b1 - hK3 * a5;
+  a[1] = c2 * it;
+  a[2] = c3 * it;
+  a[3] = c4 * it;
+  a[4] = a5;
+  const T si = I == 0 ? U : (I == 1 ? V : W);
+  R[0] += si * b1 + th * a[1 + I];
+  R[1] += si * c2;
+  R[2] += si * c3;
+  R[3] += si * c4;
+  R[4] += si * c5v + hK5t * th * a[1 + I];
+  R[1 + I] += th * (a[0] + hK5t * a5);
+}
+
+// temporal slope A = M^-1 (-R) in the co-moving frame
+template <typename T>
+HD void temporal_slope(T K, T th, T it, const T (&R)[5], T (&A)[5]) {
+  const T hK3 = T(0.5) * (K + T(3)) * th;
+  const T c5 = T(2) / ((K + T(3)) * th * th);
+  const T r1 = -R[0];
+  A[4] = c5 * (-R[4] - hK3 * r1);
+  A[0] = r1 - hK3 * A[4];
+  A[1] = -R[1] * it;
+  A[2] = -R[2] * it;
+  A[3] = -R[3] * it;
+}
+
+// Gauss-point flux, Eq. (6), local frame (u = face normal), time-linearised by the
+// closed-form two-window coefficients of Eq. (8).  Used in four calls so that the
+// caller can supply the derivative inputs lazily, one direction at a time (a callable
+// load(i, dW[5]) with i = 0 normal, 1 t1, 2 t2):
+//   begin(Wl, Wr, dt)              g_l, g_r, Q0, g0, tau = mu/p0, h
+//   add_side<+1>(load_l), add_side<-1>(load_r)   g_l H(u) and g_r (1 - H(u)) terms (Gamma_4..6)
+//   add_equilibrium(load_0)        g0 terms of Eq. (6) (Gamma_1..3)
+// Results: F (if NEED_F), dF, tau.  Invalid input propagates as NaN.
+template <typename T, bool NEED_F>
+struct GpFlux {
+  T K;
+  T rl, irl, Ul, Vl, Wl, thl, hl0, hl1;
+  T rr, irr, Ur, Vr, Wr, thr, hr0, hr1;
+  T r0, ir0, U0, V0, W0, th0;
+  T h, idt, dt;
+  T F[5], dF[5], tau;
+
+  HD void begin(const GasK<T>& g, const T (&WL)[5], const T (&WR)[5], T dt_, T idt_) {
+    K = g.K;
+    dt = dt_;
+    idt = idt_;
+    const T isqpi = T(0.56418958354775628694807945156077);  // 1/sqrt(pi)
+    const T k3 = T(4) / (K + T(3));
+    rl = WL[0];
+    irl = T(1) / rl;
+    Ul = WL[1] * irl;
+    Vl = WL[2] * irl;
+    Wl = WL[3] * irl;
+    // theta = 1/(2 lambda) = 2 (rhoE - rho|U|^2/2) / ((K+3) rho)   (A.1)
+    thl = T(0.5) * k3 * (WL[4] * irl - T(0.5) * (Ul * Ul + Vl * Vl + Wl * Wl));
+    rr = WR[0];
+    irr = T(1) / rr;
+    Ur = WR[1] * irr;
+    Vr = WR[2] * irr;
+    Wr = WR[3] * irr;
+    thr = T(0.5) * k3 * (WR[4] * irr - T(0.5) * (Ur * Ur + Vr * Vr + Wr * Wr));
+    // half-space seeds (A.2): sqrt(lambda) = sqrt(1/(2 theta))
+    const T sl = m_sqrt(T(0.5) / thl), sr = m_sqrt(T(0.5) / thr);
+    hl0 = T(0.5) * m_erfc(-sl * Ul);
+    hl1 = Ul * hl0 + T(0.5) * isqpi * m_exp(-sl * sl * Ul * Ul) / sl;
+    hr0 = T(0.5) * m_erfc(sr * Ur);
+    hr1 = Ur * hr0 - T(0.5) * isqpi * m_exp(-sr * sr * Ur * Ur) / sr;
+    // Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
+    const T hl2 = Ul * hl1 + thl * hl0, hr2 = Ur * hr1 + thr * hr0;
+    const T q0 = rl * hl0 + rr * hr0;
+    const T q1 = rl * hl1 + rr * hr1;
+    const T q2 = rl * hl0 * Vl + rr * hr0 * Vr;
+    const T q3 = rl * hl0 * Wl + rr * hr0 * Wr;
+    const T q4 = T(0.5) * (rl * (hl2 + hl0 * (Vl * Vl + Wl * Wl + (K + T(2)) * thl)) +
+                           rr * (hr2 + hr0 * (Vr * Vr + Wr * Wr + (K + T(2)) * thr)));
+    r0 = q0;
+    ir0 = T(1) / r0;
+    U0 = q1 * ir0;
+    V0 = q2 * ir0;
+    W0 = q3 * ir0;
+    th0 = T(0.5) * k3 * (q4 * ir0 - T(0.5) * (U0 * U0 + V0 * V0 + W0 * W0));
+    // tau = mu(T0)/p0 with T0 = theta0, p0 = rho0 theta0 (O-9)
+    const T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
+    tau = mu * ir0 / th0;
+    // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
+    h = m_exp(-T(0.5) * dt / tau);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      F[k] = T(0);
+      dF[k] = T(0);
+    }
+  }
+
+  // closed-form time coefficients: Gamma_1..3 (g0 terms) or Gamma_4..6 (g_l, g_r)
+  HD void gammas(bool eq, T& ga, T& gb, T& gc, T& gpa, T& gpb, T& gpc) const {
+    const T om = T(1) - h;
+    const T c13 = om * (T(3) - h) * idt;
+    const T tt = tau * tau;
+    const T idt2 = idt * idt;
+    const T gp1 = T(4) * tau * om * om * idt2;
+    const T gp2 = T(4) * tau * om * (dt * h - T(2) * tau * om) * idt2;
+    if (eq) {
+      ga = T(1) - tau * c13;
+      gb = -tau * (T(1) + T(2) * h - h * h) + T(2) * tt * c13;
+      gc = -tau + tt * c13;
+      gpa = gp1;
+      gpb = gp2;
+      gpc = T(1) - tau * gp1;
+    } else {
+      ga = tau * c13;
+      gb = tau * h * (T(2) - h) - T(2) * tt * c13;
+      gc = -tt * c13;
+      gpa = -gp1;
+      gpb = -gp2;
+      gpc = tau * gp1;
+    }
+  }
+
+  HD void accumulate(bool eq, T rho, T su, T sv, T sw, const T (&Z)[5], const T (&X)[5], const T (&Y)[5]) {
+    T ga, gb, gc, gpa, gpb, gpc;
+    gammas(eq, ga, gb, gc, gpa, gpb, gpc);
+    T d[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] = gpa * Z[k] + gpb * X[k] + gpc * Y[k];
+    shift_vec(su, sv, sw, d);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) dF[k] += rho * d[k];
+    if (NEED_F) {
+      T f[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) f[k] = ga * Z[k] + gb * X[k] + gc * Y[k];
+      shift_vec(su, sv, sw, f);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) F[k] += rho * f[k];
+    }
+  }
+
+  // g0 terms: Z = <u psi>, X = sum_i <u u_i a_i.psi psi>, Y = <u A.psi psi> (full space), in the
+  // co-moving frame: Z = U0 m0 + theta e2, Y = -U0 R + Q_x(A),
+  // X = U0 R + sum_i (s_i Q_x(a_i) + P_xi(a_i)) with P_xi(a) = <c_x c_i (a.psi) psi>.
+  template <class Load>
+  HD void add_equilibrium(Load&& load) {
+    const T th = th0, it = T(1) / th0;
+    const T hK3 = T(0.5) * (K + T(3)) * th;
+    const T hK5t = T(0.5) * (K + T(5)) * th;
+    const T t2 = th * th;
+    T R[5] = {T(0), T(0), T(0), T(0), T(0)};
+    T X[5] = {T(0), T(0), T(0), T(0), T(0)};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      T dW[5], a[5];
+      load(i, dW);
+      if (i == 0) slope_dir<0>(K, ir0, U0, V0, W0, th, it, dW, a, R);
+      if (i == 1) slope_dir<1>(K, ir0, U0, V0, W0, th, it, dW, a, R);
+      if (i == 2) slope_dir<2>(K, ir0, U0, V0, W0, th, it, dW, a, R);
+      const T si = i == 0 ? U0 : (i == 1 ? V0 : W0);
+      // s_i Q_x(a)
+      X[0] += si * th * a[1];
+      X[1] += si * th * (a[0] + hK5t * a[4]);
+      X[4] += si * hK5t * th * a[1];
+      if (i == 0) {  // P_xx(a)
+        X[0] += th * (a[0] + hK5t * a[4]);
+        X[1] += T(3) * t2 * a[1];
+        X[2] += t2 * a[2];
+        X[3] += t2 * a[3];
+        X[4] += hK5t * th * (a[0] + T(0.5) * (K + T(7)) * th * a[4]);
+      } else if (i == 1) {  // P_xy(a)
+        X[1] += t2 * a[2];
+        X[2] += t2 * a[1];
+      } else {  // P_xz(a)
+        X[1] += t2 * a[3];
+        X[3] += t2 * a[1];
+      }
+    }
+    T A[5];
+    temporal_slope(K, th, it, R, A);
+    T Y[5];
+    Y[0] = -U0 * R[0] + th * A[1];
+    Y[1] = -U0 * R[1] + th * (A[0] + hK5t * A[4]);
+    Y[2] = -U0 * R[2];
+    Y[3] = -U0 * R[3];
+    Y[4] = -U0 * R[4] + hK5t * th * A[1];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) X[k] += U0 * R[k];
+    T Z[5] = {U0, th, T(0), T(0), U0 * hK3};
+    accumulate(true, r0, U0, V0, W0, Z, X, Y);
+  }
+
+  // g_l on u > 0 (SIDE = +1) or g_r on u < 0 (SIDE = -1): half-space u-moments t_n, frame moving
+  // with the tangential velocity (V, W) only.
+  template <int SIDE, class Load>
+  HD void add_side(Load&& load) {
+    const T rho = SIDE > 0 ? rl : rr, irho = SIDE > 0 ? irl : irr;
+    const T U = SIDE > 0 ? Ul : Ur, V = SIDE > 0 ? Vl : Vr, W = SIDE > 0 ? Wl : Wr;
+    const T th = SIDE > 0 ? thl : thr, it = T(1) / th;
+    // half-space u-moments t_0..t_6 (A.2 recursion)
+    T t[7];
+    t[0] = SIDE > 0 ? hl0 : hr0;
+    t[1] = SIDE > 0 ? hl1 : hr1;
+#pragma unroll
+    for (int n = 0; n + 2 < 7; ++n) t[n + 2] = U * t[n + 1] + T(n + 1) * th * t[n];
+    const T k2 = (K + T(2)) * th, k4 = (K + T(4)) * th;
+    const T hU2 = T(0.5) * U * U;
+    auto e = [&](const T (&al)[5], int n) { return al[0] * t[n] + al[1] * t[n + 1] + T(0.5) * al[4] * (t[n + 2] + k2 * t[n]); };
+    auto f = [&](const T (&al)[5], int n) { return al[0] * t[n] + al[1] * t[n + 1] + T(0.5) * al[4] * (t[n + 2] + k4 * t[n]); };
+    // out += wgt H_n(al),  H_n(al) = <u^n (al.psi) psi>_t
+    auto H = [&](const T (&al)[5], int n, T wgt, T (&out)[5]) {
+      out[0] += wgt * e(al, n);
+      out[1] += wgt * e(al, n + 1);
+      out[2] += wgt * al[2] * th * t[n];
+      out[3] += wgt * al[3] * th * t[n];
+      out[4] += wgt * T(0.5) * (e(al, n + 2) + k2 * f(al, n));
+    };
+    // to the tangential frame: alpha_t = T(-U,0,0)^T alpha_c
+    auto to_t = [&](T (&al)[5]) {
+      al[0] += -U * al[1] + hU2 * al[4];
+      al[1] += -U * al[4];
+    };
+    T R[5] = {T(0), T(0), T(0), T(0), T(0)};
+    T X[5] = {T(0), T(0), T(0), T(0), T(0)};
+    const T g3 = T(0.5) * th * (t[3] + k4 * t[1]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      T dW[5], a[5];
+      load(i, dW);
+      if (i == 0) slope_dir<0>(K, irho, U, V, W, th, it, dW, a, R);
+      if (i == 1) slope_dir<1>(K, irho, U, V, W, th, it, dW, a, R);
+      if (i == 2) slope_dir<2>(K, irho, U, V, W, th, it, dW, a, R);
+      to_t(a);
+      if (i == 0) {
+        H(a, 2, T(1), X);
+      } else if (i == 1) {  // V H_1(a) + G_v(a)
+        H(a, 1, V, X);
+        X[0] += th * t[1] * a[2];
+        X[1] += th * t[2] * a[2];
+        X[2] += th * f(a, 1);
+        X[4] += g3 * a[2];
+      } else {  // W H_1(a) + G_w(a)
+        H(a, 1, W, X);
+        X[0] += th * t[1] * a[3];
+        X[1] += th * t[2] * a[3];
+        X[3] += th * f(a, 1);
+        X[4] += g3 * a[3];
+      }
+    }
+    T A[5];
+    temporal_slope(K, th, it, R, A);
+    to_t(A);
+    T Y[5] = {T(0), T(0), T(0), T(0), T(0)};
+    H(A, 1, T(1), Y);
+    T Z[5] = {t[1], t[2], T(0), T(0), T(0.5) * (t[3] + k2 * t[1])};
+    accumulate(false, rho, T(0), V, W, Z, X, Y);
+  }
 };
 
-template <int N, typename T>
-__device__ __forceinline__ void recur(T* m, T U, T th) {  // m[n+2] = U m[n+1] + (n+1) th m[n]
-#pragma unroll
-  for (int n = 0; n + 2 < N; ++n) m[n + 2] = U * m[n + 1] + T(n + 1) * th * m[n];
-}
-
-// S(a,b,c) = <u^a v^b w^c (alpha.psi)>
-template <int a, int b, int c, typename T>
-__device__ __forceinline__ T S_(const Tab<T>& t, const T (&al)[5]) {
-  const T uvw = t.u[a] * t.v[b] * t.w[c];
-  return al[0] * uvw + al[1] * (t.u[a + 1] * t.v[b] * t.w[c]) + al[2] * (t.u[a] * t.v[b + 1] * t.w[c]) +
-         al[3] * (t.u[a] * t.v[b] * t.w[c + 1]) +
-         T(0.5) * al[4] *
-             (t.u[a + 2] * t.v[b] * t.w[c] + t.u[a] * t.v[b + 2] * t.w[c] + t.u[a] * t.v[b] * t.w[c + 2] +
-              uvw * t.x1);
-}
-// Sx(a,b,c) = <u^a v^b w^c xi^2 (alpha.psi)>
-template <int a, int b, int c, typename T>
-__device__ __forceinline__ T Sx_(const Tab<T>& t, const T (&al)[5]) {
-  const T uvw = t.u[a] * t.v[b] * t.w[c];
-  return t.x1 * (al[0] * uvw + al[1] * (t.u[a + 1] * t.v[b] * t.w[c]) + al[2] * (t.u[a] * t.v[b + 1] * t.w[c]) +
-                 al[3] * (t.u[a] * t.v[b] * t.w[c + 1]) +
-                 T(0.5) * al[4] * (t.u[a + 2] * t.v[b] * t.w[c] + t.u[a] * t.v[b + 2] * t.w[c] + t.u[a] * t.v[b] * t.w[c + 2])) +
-         T(0.5) * al[4] * uvw * t.x2;
-}
-// out += <u^a v^b w^c (alpha.psi) psi>
-template <int a, int b, int c, typename T>
-__device__ __forceinline__ void polypsi_acc(const Tab<T>& t, const T (&al)[5], T (&out)[5]) {
-  out[0] += S_<a, b, c>(t, al);
-  out[1] += S_<a + 1, b, c>(t, al);
-  out[2] += S_<a, b + 1, c>(t, al);
-  out[3] += S_<a, b, c + 1>(t, al);
-  out[4] += T(0.5) * (S_<a + 2, b, c>(t, al) + S_<a, b + 2, c>(t, al) + S_<a, b, c + 2>(t, al) + Sx_<a, b, c>(t, al));
-}
-
-// Closed-form inverse of the compatibility matrix: solves <(a.psi) psi> = b for
-// the Maxwellian (U, V, W, lambda).  Sq = U^2+V^2+W^2+(K+3)/(2 lambda), tl = 2 lambda,
-// c5 = 4 lambda^2/(K+3).
-template <typename T>
-__device__ __forceinline__ void minv(T U, T V, T W, T Sq, T tl, T c5, const T (&b)[5], T (&a)[5]) {
-  T R4 = T(2) * b[4] - Sq * b[0];
-  T R1 = b[1] - U * b[0], R2 = b[2] - V * b[0], R3 = b[3] - W * b[0];
-  a[4] = c5 * (R4 - T(2) * (U * R1 + V * R2 + W * R3));
-  a[3] = tl * R3 - W * a[4];
-  a[2] = tl * R2 - V * a[4];
-  a[1] = tl * R1 - U * a[4];
-  a[0] = b[0] - U * a[1] - V * a[2] - W * a[3] - T(0.5) * a[4] * Sq;
-}
-
-// Contribution of one Maxwellian g (density rho, velocity U,V,W, lambda) with conservative
-// derivatives dW[i] (i: normal, t1, t2) to the flux:
-//   F  += rho (Ga Z + Gb X + Gc Y),   dF += rho (Gpa Z + Gpb X + Gpc Y)
-// with Z = <u psi>, X = <u^2 a1.psi psi> + <u v a2.psi psi> + <u w a3.psi psi>, Y = <u A.psi psi>
-// over the u-range WHICH (0: full, +1: u>0, -1: u<0) — the g0 terms (Ga..Gc = Gamma_1..3) and
-// the g_l / g_r terms (Gamma_4..6) of Eq. (6).  Slopes a_i from <a_i> = dW_i/rho (O-7) and A from
-// <u a1.psi + v a2.psi + w a3.psi + A.psi> = 0 on the FULL space.
-// h0, h1: half-space <u^0>, <u^1> of this Maxwellian (unused when WHICH == 0).
-template <typename T, int WHICH, bool NEED_F>
-__device__ __forceinline__ void maxwellian_contrib(T K, T rho, T U, T V, T W, T lam, const T (&dW)[3][5],
-                                                   T h0, T h1, T Ga, T Gb, T Gc, T Gpa, T Gpb, T Gpc,
-                                                   T (&F)[5], T (&dF)[5]) {
-  Tab<T> t;
-  const T th = T(0.5) / lam;  // 1/(2 lambda)
-  t.u[0] = T(1); t.u[1] = U; recur<7>(t.u, U, th);
-  t.v[0] = T(1); t.v[1] = V; recur<6>(t.v, V, th);
-  t.w[0] = T(1); t.w[1] = W; recur<6>(t.w, W, th);
-  t.x1 = K * th;
-  t.x2 = K * (K + T(2)) * th * th;
-  const T Sq = U * U + V * V + W * W + (K + T(3)) * th;
-  const T tl = T(2) * lam;
-  const T c5 = T(4) * lam * lam / (K + T(3));
-  const T irho = T(1) / rho;
-
-  T a[3][5];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    T b[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) b[k] = dW[i][k] * irho;
-    minv(U, V, W, Sq, tl, c5, b, a[i]);
-  }
-  T A[5];
-  {
-    T R[5] = {T(0), T(0), T(0), T(0), T(0)};
-    polypsi_acc<1, 0, 0>(t, a[0], R);
-    polypsi_acc<0, 1, 0>(t, a[1], R);
-    polypsi_acc<0, 0, 1>(t, a[2], R);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) R[k] = -R[k];
-    minv(U, V, W, Sq, tl, c5, R, A);
-  }
-  if (WHICH != 0) {  // switch the u-table to the half space
-    t.u[0] = h0;
-    t.u[1] = h1;
-    recur<7>(t.u, U, th);
-  }
-  T X[5] = {T(0), T(0), T(0), T(0), T(0)};
-  polypsi_acc<2, 0, 0>(t, a[0], X);
-  polypsi_acc<1, 1, 0>(t, a[1], X);
-  polypsi_acc<1, 0, 1>(t, a[2], X);
-  T Y[5] = {T(0), T(0), T(0), T(0), T(0)};
-  polypsi_acc<1, 0, 0>(t, A, Y);
-  T Z[5];
-  Z[0] = t.u[1];
-  Z[1] = t.u[2];
-  Z[2] = t.u[1] * t.v[1];
-  Z[3] = t.u[1] * t.w[1];
-  Z[4] = T(0.5) * (t.u[3] + t.u[1] * (t.v[2] + t.w[2] + t.x1));
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    if (NEED_F) F[k] += rho * (Ga * Z[k] + Gb * X[k] + Gc * Y[k]);
-    dF[k] += rho * (Gpa * Z[k] + Gpb * X[k] + Gpc * Y[k]);
-  }
-}
-
-// Gauss-point flux in the local frame (u along the face normal).  Inputs as in the oracle:
-// Wl, Wr conservative states; dWl/dWr/dW0 [i][k] derivatives along (normal, t1, t2).
-// Returns F^n (if NEED_F) and d_t F^n, and tau.  Invalid input propagates as NaN.
+// One-call form (tests and the batched test entry point).
 template <typename T, bool NEED_F>
-__device__ __forceinline__ void gp_flux(const GasK<T>& g, const T (&Wl)[5], const T (&Wr)[5],
-                                        const T (&dWl)[3][5], const T (&dWr)[3][5], const T (&dW0)[3][5],
-                                        T dt, T (&F)[5], T (&dF)[5], T& tau) {
-  const T K = g.K;
-  const T isqpi = T(0.56418958354775628694807945156077);  // 1/sqrt(pi)
-  // left / right Maxwellians (A.1)
-  T rl = Wl[0], irl = T(1) / rl;
-  T Ul = Wl[1] * irl, Vl = Wl[2] * irl, Wl3 = Wl[3] * irl;
-  T laml = (K + T(3)) * rl / (T(4) * (Wl[4] - T(0.5) * rl * (Ul * Ul + Vl * Vl + Wl3 * Wl3)));
-  T rr = Wr[0], irr = T(1) / rr;
-  T Ur = Wr[1] * irr, Vr = Wr[2] * irr, Wr3 = Wr[3] * irr;
-  T lamr = (K + T(3)) * rr / (T(4) * (Wr[4] - T(0.5) * rr * (Ur * Ur + Vr * Vr + Wr3 * Wr3)));
-  // half-space seeds (A.2): <u^0>_{>0}, <u^1>_{>0} of g_l; <u^0>_{<0}, <u^1>_{<0} of g_r
-  T sl = m_sqrt(laml), sr = m_sqrt(lamr);
-  T hl0 = T(0.5) * m_erfc(-sl * Ul);
-  T hl1 = Ul * hl0 + T(0.5) * isqpi * m_exp(-laml * Ul * Ul) / sl;
-  T hr0 = T(0.5) * m_erfc(sr * Ur);
-  T hr1 = Ur * hr0 - T(0.5) * isqpi * m_exp(-lamr * Ur * Ur) / sr;
-  // Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
-  T thl = T(0.5) / laml, thr = T(0.5) / lamr;
-  T hl2 = Ul * hl1 + thl * hl0, hr2 = Ur * hr1 + thr * hr0;
-  T Q0[5];
-  Q0[0] = rl * hl0 + rr * hr0;
-  Q0[1] = rl * hl1 + rr * hr1;
-  Q0[2] = rl * hl0 * Vl + rr * hr0 * Vr;
-  Q0[3] = rl * hl0 * Wl3 + rr * hr0 * Wr3;
-  Q0[4] = T(0.5) * (rl * (hl2 + hl0 * (Vl * Vl + Wl3 * Wl3 + (K + T(2)) * thl)) +
-                    rr * (hr2 + hr0 * (Vr * Vr + Wr3 * Wr3 + (K + T(2)) * thr)));
-  T r0 = Q0[0], ir0 = T(1) / r0;
-  T U0 = Q0[1] * ir0, V0 = Q0[2] * ir0, W0 = Q0[3] * ir0;
-  T lam0 = (K + T(3)) * r0 / (T(4) * (Q0[4] - T(0.5) * r0 * (U0 * U0 + V0 * V0 + W0 * W0)));
-  // tau = mu/p0 (O-9)
-  T T0 = T(0.5) / lam0;
-  T p0 = r0 * T0;
-  T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(T0 / g.T_ref, g.omega) : g.mu_ref;
-  tau = mu / p0;
-  // closed-form time coefficients, h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
-  T h = m_exp(-dt / (T(2) * tau));
-  T om = T(1) - h, idt = T(1) / dt;
-  T c13 = om * (T(3) - h) * idt;
-  T tt = tau * tau;
-  T G1 = T(1) - tau * c13;
-  T G2 = -tau * (T(1) + T(2) * h - h * h) + T(2) * tt * c13;
-  T G3 = -tau + tt * c13;
-  T G4 = tau * c13;
-  T G5 = tau * h * (T(2) - h) - T(2) * tt * c13;
-  T G6 = -tt * c13;
-  T idt2 = idt * idt;
-  T Gp1 = T(4) * tau * om * om * idt2;
-  T Gp2 = T(4) * tau * om * (dt * h - T(2) * tau * om) * idt2;
-  T Gp3 = T(1) - T(4) * tt * om * om * idt2;
-  T Gp4 = -Gp1, Gp5 = -Gp2, Gp6 = tau * Gp1;
-
+HD void gp_flux(const GasK<T>& g, const T (&Wl)[5], const T (&Wr)[5], const T (&dWl)[3][5], const T (&dWr)[3][5],
+                const T (&dW0)[3][5], T dt, T (&F)[5], T (&dF)[5], T& tau) {
+  GpFlux<T, NEED_F> gf;
+  gf.begin(g, Wl, Wr, dt, T(1) / dt);
+  gf.template add_side<+1>([&](int i, T (&d)[5]) { for (int k = 0; k < 5; ++k) d[k] = dWl[i][k]; });
+  gf.template add_side<-1>([&](int i, T (&d)[5]) { for (int k = 0; k < 5; ++k) d[k] = dWr[i][k]; });
+  gf.add_equilibrium([&](int i, T (&d)[5]) { for (int k = 0; k < 5; ++k) d[k] = dW0[i][k]; });
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
-    F[k] = T(0);
-    dF[k] = T(0);
+    F[k] = gf.F[k];
+    dF[k] = gf.dF[k];
   }
-  maxwellian_contrib<T, 0, NEED_F>(K, r0, U0, V0, W0, lam0, dW0, T(0), T(0), G1, G2, G3, Gp1, Gp2, Gp3, F, dF);
-  maxwellian_contrib<T, 1, NEED_F>(K, rl, Ul, Vl, Wl3, laml, dWl, hl0, hl1, G4, G5, G6, Gp4, Gp5, Gp6, F, dF);
-  maxwellian_contrib<T, -1, NEED_F>(K, rr, Ur, Vr, Wr3, lamr, dWr, hr0, hr1, G4, G5, G6, Gp4, Gp5, Gp6, F, dF);
+  tau = gf.tau;
 }
 
 }  // namespace hgks

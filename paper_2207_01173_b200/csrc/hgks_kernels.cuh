@@ -47,32 +47,46 @@ __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, 
   return (long long)(k + 3) * g.plane + (long long)v * g.vs + (long long)(j + 3) * g.px + (i + 3);
 }
 
+#ifndef HGKS_FLUX_MINB
+#define HGKS_FLUX_MINB 2  // resident flux blocks per SM (register budget 128/thread)
+#endif
 constexpr int TT1 = 8, TT2 = 8;            // faces per tile along t1, t2
 constexpr int TL1 = TT1 + 4, TL2 = TT2 + 4;  // lines per tile (+-2 tangential halo)
 constexpr int NTHREADS_FLUX = TT1 * TT2 * 4;
 constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
+// shared-memory strides (in elements), padded so that half-warps hit 16 distinct 8-byte banks
+constexpr int SA_C = TL2 * TL1 + 8;          // one (field, component) plane of sA: 152
+constexpr int SB_K = 2 * TT1;                // one slot k of sB: (m, a) = 16
+constexpr int SB_RC = NB * SB_K + 8;         // one (row, component) block of sB: 152
 
 template <typename T>
 constexpr size_t flux_smem_bytes() {
-  return sizeof(T) * (6 * 5 * TL2 * TL1 + TT1 * TL2 * 2 * 5 * NB);
+  return sizeof(T) * (6 * 5 * SA_C + TL2 * 5 * SB_RC);
 }
 
+// Fused flux sweep of one direction for one tile of TT1 x TT2 faces at normal face index fn:
+//   A  normal reconstruction (A2) of the (TT1+4) x (TT2+4) lines -> sA[field][comp][l2][l1]
+//   B  t1 pass (A3): values at the two t1 Gauss abscissae of all 6 fields and t1-derivatives of
+//      Ql, Qr, C on every row -> sB[l2][comp][slot][m][a]
+//   C  one thread per Gauss point: t2 pass, loaded lazily one derivative direction at a time,
+//      feeding the BGK flux (A4-A6); 4-point quadrature by warp shuffles (A7)
+// Lane layout in phase C: lane = 16 n + 8 m + a (a = t1 face in tile, (m, n) the Gauss point),
+// warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
 template <typename T, int DIR, int STAGE>
-__global__ void __launch_bounds__(NTHREADS_FLUX, 1)
+__global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     flux_kernel(const T* __restrict__ q, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sA = reinterpret_cast<T*>(smem_raw);     // [6][5][TL2][TL1]
-  T* sB = sA + 6 * 5 * TL2 * TL1;             // [TT1][TL2][2][5][NB]
+  T* sA = reinterpret_cast<T*>(smem_raw);  // [6][5][SA_C]
+  T* sB = sA + 6 * 5 * SA_C;               // [TL2][5][SB_RC]
 
-  const int nN = g.n[DIR], n1 = g.n[A1], n2 = g.n[A2];
+  const int n1 = g.n[A1], n2 = g.n[A2];
   const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2, fn = blockIdx.z;  // face fn: cells fn-1 | fn
   const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
   const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
   const long long s2 = (A2 == 0) ? 1 : (A2 == 1 ? g.px : g.plane);
   const T ihN = g.ih[DIR];
-  (void)nN;
 
   // ---- phase A: normal reconstruction of TL1 x TL2 lines, 5 components --------------------
   for (int w = threadIdx.x; w < TL1 * TL2 * 5; w += NTHREADS_FLUX) {
@@ -85,95 +99,122 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, 1)
     g2 = min(max(g2, -3), n2 + 2);
     const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 1 + DIR : (c == 2 ? 1 + A1 : 1 + A2)));
     // cell (fn - 3) along the normal, (g1, g2) tangentially; interior index origin at +3 ghosts
-    long long base = 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs + (long long)(fn - 3) * sN + g1 * s1 + g2 * s2;
+    const long long base =
+        3LL * (g.plane + g.px + 1) + (long long)gv * g.vs + (long long)(fn - 3) * sN + g1 * s1 + g2 * s2;
     T s[6];
 #pragma unroll
     for (int r = 0; r < 6; ++r) s[r] = q[base + r * sN];
     T f[6];
     normal_fields(s, ihN, f);
 #pragma unroll
-    for (int ff = 0; ff < 6; ++ff) sA[((ff * 5 + c) * TL2 + l2) * TL1 + l1] = f[ff];
+    for (int ff = 0; ff < 6; ++ff) sA[(ff * 5 + c) * SA_C + l2 * TL1 + l1] = f[ff];
   }
   __syncthreads();
 
   // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
-  for (int w = threadIdx.x; w < TT1 * TL2 * 2 * 5; w += NTHREADS_FLUX) {
-    const int c = w % 5;
-    int rest = w / 5;
-    const int m = rest % 2;
-    rest /= 2;
+  // Gauss point m = 1 uses the mirrored weights: wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
+  for (int w = threadIdx.x; w < TT1 * 5 * TL2 * 2; w += NTHREADS_FLUX) {
+    const int a = w % TT1;
+    const int c = (w / TT1) % 5;
+    const int rest = w / (TT1 * 5);
     const int l2 = rest % TL2;
-    const int a = rest / TL2;
+    const int m = rest / TL2;
     T out[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) out[k] = T(0);
+    const T* src = sA + c * SA_C + l2 * TL1 + a;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const T wv = T(kWV[m][r]), wd = T(kWD[m][r]);
+      const int rr = m ? 4 - r : r;
+      const T wv = T(kWV0(r)), wd = T(kWD0(r));
 #pragma unroll
       for (int ff = 0; ff < 6; ++ff) {
-        const T x = sA[((ff * 5 + c) * TL2 + l2) * TL1 + a + r];
+        const T x = src[ff * 5 * SA_C + rr];
         out[ff] += wv * x;
         if (ff == 0) out[6] += wd * x;
         if (ff == 1) out[7] += wd * x;
         if (ff == 4) out[8] += wd * x;
       }
     }
-    T* dst = sB + ((((a * TL2 + l2) * 2 + m) * 5 + c) * NB);
+    const T sg = m ? T(-1) : T(1);
+    out[6] *= sg;
+    out[7] *= sg;
+    out[8] *= sg;
+    T* dst = sB + (l2 * 5 + c) * SB_RC + m * TT1 + a;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) dst[k] = out[k];
+    for (int k = 0; k < NB; ++k) dst[k * SB_K] = out[k];
   }
   __syncthreads();
 
-  // ---- phase C: one thread per Gauss point --------------------------------------------------
-  const int gp = threadIdx.x & 3, face = threadIdx.x >> 2;
-  const int m = gp >> 1, nn = gp & 1;
-  const int a = face % TT1, b = face / TT1;
+  // ---- phase C: one thread per Gauss point ----------------------------------------------------
+  const int lane = threadIdx.x & 31;
+  const int a = lane & 7, m = (lane >> 3) & 1, nn = lane >> 4;
+  const int b = threadIdx.x >> 5;
   const T ih1 = g.ih[A1], ih2 = g.ih[A2];
-  T Wl[5], Wr[5], dWl[3][5], dWr[3][5], dW0[3][5];
+  const T sgn = nn ? T(-1) : T(1);
+  // row r of this Gauss point's 5-row t2 stencil: rows b..b+4, mirrored for n = 1
+  const T* row0 = sB + m * TT1 + a + (b + (nn ? 4 : 0)) * (5 * SB_RC);
+  const int rstep = nn ? -5 * SB_RC : 5 * SB_RC;
+  // t2 pass of slot k, component c: value (wv) or derivative (wd).  The empty asm with a memory
+  // clobber keeps ptxas from hoisting these shared loads ahead of earlier flux work (register
+  // pressure: they would be spilled).
+  auto tv = [&](int c, int k) {
+    asm volatile("" ::: "memory");
+    T v = T(0);
 #pragma unroll
-  for (int c = 0; c < 5; ++c) {
-    T v[NB];
-    T d2[3];
+    for (int r = 0; r < 5; ++r) v += T(kWV0(r)) * row0[r * rstep + c * SB_RC + k * SB_K];
+    return v;
+  };
+  auto td = [&](int c, int k) {
+    asm volatile("" ::: "memory");
+    T v = T(0);
 #pragma unroll
-    for (int k = 0; k < NB; ++k) v[k] = T(0);
-    d2[0] = d2[1] = d2[2] = T(0);
+    for (int r = 0; r < 5; ++r) v += T(kWD0(r)) * row0[r * rstep + c * SB_RC + k * SB_K];
+    return sgn * v;
+  };
+  const T dt = T(ctl->dt);
+  GpFlux<T, STAGE == 1> gf;
+  {
+    T Wl[5], Wr[5];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const T wv = T(kWV[nn][r]), wd = T(kWD[nn][r]);
-      const T* src = sB + ((((a * TL2 + b + r) * 2 + m) * 5 + c) * NB);
-#pragma unroll
-      for (int k = 0; k < NB; ++k) v[k] += wv * src[k];
-      d2[0] += wd * src[0];
-      d2[1] += wd * src[1];
-      d2[2] += wd * src[4];
+    for (int c = 0; c < 5; ++c) {
+      Wl[c] = tv(c, 0);
+      Wr[c] = tv(c, 1);
     }
-    Wl[c] = v[0];
-    Wr[c] = v[1];
-    dWl[0][c] = v[2];
-    dWr[0][c] = v[3];
-    dW0[0][c] = v[5];
-    dWl[1][c] = v[6] * ih1;
-    dWr[1][c] = v[7] * ih1;
-    dW0[1][c] = v[8] * ih1;
-    dWl[2][c] = d2[0] * ih2;
-    dWr[2][c] = d2[1] * ih2;
-    dW0[2][c] = d2[2] * ih2;
+    gf.begin(gas, Wl, Wr, dt, T(1) / dt);
   }
-  T F[5], dF[5], tau;
-  gp_flux<T, STAGE == 1>(gas, Wl, Wr, dWl, dWr, dW0, T(ctl->dt), F, dF, tau);
-  // 2x2 Gauss quadrature, omega_mn = 1/4 (O-8): lanes 4f..4f+3 hold the face's Gauss points
+  // derivative inputs, one direction at a time: normal (value of dQ/dn or D), t1 (D1 slots),
+  // t2 (t2-derivative of Ql, Qr or C)
+  gf.template add_side<+1>([&](int i, T (&d)[5]) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 2) : (i == 1 ? tv(c, 6) * ih1 : td(c, 0) * ih2);
+  });
+  gf.template add_side<-1>([&](int i, T (&d)[5]) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 3) : (i == 1 ? tv(c, 7) * ih1 : td(c, 1) * ih2);
+  });
+  gf.add_equilibrium([&](int i, T (&d)[5]) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 5) : (i == 1 ? tv(c, 8) * ih1 : td(c, 4) * ih2);
+  });
+  T F[5], dF[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    F[k] = gf.F[k];
+    dF[k] = gf.dF[k];
+  }
+  // 2x2 Gauss quadrature, omega_mn = 1/4 (O-8): the face's Gauss points sit at lanes a, a+8, a+16, a+24
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
     if (STAGE == 1) {
-      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 1);
-      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 2);
+      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 8);
+      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 16);
     }
-    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 1);
-    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 2);
+    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 8);
+    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 16);
   }
   const int f1 = t10 + a, f2 = t20 + b;
-  if (gp == 0 && f1 < n1 && f2 < n2) {
+  if (lane < 8 && f1 < n1 && f2 < n2) {
     int cd[3];
     cd[DIR] = fn;
     cd[A1] = f1;

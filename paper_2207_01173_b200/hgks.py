@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhgks.so")
+LIB_PATH = os.environ.get("HGKS_LIB") or os.path.join(PKG, "libhgks.so")
 
 HGKS_OK, HGKS_EINVAL, HGKS_ECUDA, HGKS_ENCCL, HGKS_ESTATE, HGKS_ENOMEM = 0, -1, -2, -3, -4, -5
 HGKS_FP64, HGKS_FP32 = 0, 1
