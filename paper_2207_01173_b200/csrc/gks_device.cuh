@@ -34,6 +34,37 @@ __host__ __device__ __forceinline__ float m_pow(float x, float y) { return powf(
 __host__ __device__ __forceinline__ double m_abs(double x) { return fabs(x); }
 __host__ __device__ __forceinline__ float m_abs(float x) { return fabsf(x); }
 
+// Reciprocal / quotient without the IEEE slow path: MUFU seed (rcp.approx) refined by Newton steps
+// (two for fp64: 23 -> 46 -> full 53 bits; the residual-corrected quotient is within 1 ulp of the
+// IEEE result for the normal-range operands the scheme produces).  Host builds use plain division.
+__host__ __device__ __forceinline__ double rcp(double x) {
+#ifdef __CUDA_ARCH__
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+#else
+  return 1.0 / x;
+#endif
+}
+__host__ __device__ __forceinline__ float rcp(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return fmaf(y, fmaf(-x, y, 1.0f), y);
+#else
+  return 1.0f / x;
+#endif
+}
+template <typename T>
+__host__ __device__ __forceinline__ T qdiv(T a, T b) {  // a / b, residual-corrected
+  const T y = rcp(b);
+  const T q = a * y;
+  return q + y * (a - b * q);
+}
+
 template <typename T>
 struct GasK {
   T K;       // internal degrees of freedom, computed in fp64 on the host (O-20)
@@ -51,29 +82,36 @@ template <typename T>
 __device__ __forceinline__ void weno5z_cell(T s0, T s1, T s2, T s3, T s4, T& left, T& right) {
   const T eps = T(1e-16);
   const T c13 = T(13.0 / 12.0);
-  T d0 = s0 - T(2) * s1 + s2, e0 = s0 - T(4) * s1 + T(3) * s2;
-  T d1 = s1 - T(2) * s2 + s3, e1 = s1 - s3;
-  T d2 = s2 - T(2) * s3 + s4, e2 = T(3) * s2 - T(4) * s3 + s4;
-  T b0 = c13 * d0 * d0 + T(0.25) * e0 * e0;
-  T b1 = c13 * d1 * d1 + T(0.25) * e1 * e1;
-  T b2 = c13 * d2 * d2 + T(0.25) * e2 * e2;
-  T t5 = m_abs(b0 - b2);
-  T r0 = t5 / (b0 + eps), r1 = t5 / (b1 + eps), r2 = t5 / (b2 + eps);
-  T q0 = T(1) + r0 * r0, q1 = T(1) + r1 * r1, q2 = T(1) + r2 * r2;
+  const T d0 = s0 - T(2) * s1 + s2, e0 = s0 - T(4) * s1 + T(3) * s2;
+  const T d1 = s1 - T(2) * s2 + s3, e1 = s1 - s3;
+  const T d2 = s2 - T(2) * s3 + s4, e2 = T(3) * s2 - T(4) * s3 + s4;
+  const T D0 = c13 * d0 * d0 + T(0.25) * e0 * e0 + eps;  // beta_k + eps
+  const T D1 = c13 * d1 * d1 + T(0.25) * e1 * e1 + eps;
+  const T D2 = c13 * d2 * d2 + T(0.25) * e2 * e2 + eps;
+  const T t5 = m_abs(D0 - D2);
   const T sixth = T(1.0 / 6.0);
-  {  // right edge x_{i+1/2}
-    T a0 = T(0.1) * q0, a1 = T(0.6) * q1, a2 = T(0.3) * q2;
-    T p0 = (T(2) * s0 - T(7) * s1 + T(11) * s2) * sixth;
-    T p1 = (-s1 + T(5) * s2 + T(2) * s3) * sixth;
-    T p2 = (T(2) * s2 + T(5) * s3 - s4) * sixth;
-    right = (a0 * p0 + a1 * p1 + a2 * p2) / (a0 + a1 + a2);
-  }
-  {  // left edge x_{i-1/2}: stencil reversed, beta0 <-> beta2
-    T a0 = T(0.1) * q2, a1 = T(0.6) * q1, a2 = T(0.3) * q0;
-    T p0 = (T(2) * s4 - T(7) * s3 + T(11) * s2) * sixth;
-    T p1 = (-s3 + T(5) * s2 + T(2) * s1) * sixth;
-    T p2 = (T(2) * s2 + T(5) * s1 - s0) * sixth;
-    left = (a0 * p0 + a1 * p1 + a2 * p2) / (a0 + a1 + a2);
+  const T p0 = (T(2) * s0 - T(7) * s1 + T(11) * s2) * sixth;  // right-edge candidates
+  const T p1 = (-s1 + T(5) * s2 + T(2) * s3) * sixth;
+  const T p2 = (T(2) * s2 + T(5) * s3 - s4) * sixth;
+  const T m0 = (T(2) * s4 - T(7) * s3 + T(11) * s2) * sixth;  // left-edge candidates (mirror)
+  const T m1 = (-s3 + T(5) * s2 + T(2) * s1) * sixth;
+  const T m2 = (T(2) * s2 + T(5) * s1 - s0) * sixth;
+  if (sizeof(T) == 8) {
+    // alpha_k = d_k (1 + (tau5/D_k)^2) = d_k (D_k^2 + tau5^2)/D_k^2: scale every alpha by
+    // D0^2 D1^2 D2^2 (in fp64 range: 1e-96 <= product <= 1e18) so each edge needs one quotient
+    const T D0s = D0 * D0, D1s = D1 * D1, D2s = D2 * D2, ts = t5 * t5;
+    const T n0 = (D0s + ts) * (D1s * D2s), n1 = (D1s + ts) * (D0s * D2s), n2 = (D2s + ts) * (D0s * D1s);
+    const T a0 = T(0.1) * n0, a1 = T(0.6) * n1, a2 = T(0.3) * n2;   // right edge weights (1,6,3)/10
+    right = qdiv(a0 * p0 + a1 * p1 + a2 * p2, a0 + a1 + a2);
+    const T b0 = T(0.1) * n2, b1 = T(0.6) * n1, b2 = T(0.3) * n0;   // left edge: beta0 <-> beta2
+    left = qdiv(b0 * m0 + b1 * m1 + b2 * m2, b0 + b1 + b2);
+  } else {
+    const T r0 = t5 * rcp(D0), r1 = t5 * rcp(D1), r2 = t5 * rcp(D2);
+    const T q0 = T(1) + r0 * r0, q1 = T(1) + r1 * r1, q2 = T(1) + r2 * r2;
+    const T a0 = T(0.1) * q0, a1 = T(0.6) * q1, a2 = T(0.3) * q2;
+    right = qdiv(a0 * p0 + a1 * p1 + a2 * p2, a0 + a1 + a2);
+    const T b0 = T(0.1) * q2, b1 = T(0.6) * q1, b2 = T(0.3) * q0;
+    left = qdiv(b0 * m0 + b1 * m1 + b2 * m2, b0 + b1 + b2);
   }
 }
 
@@ -150,7 +188,7 @@ HD void shift_vec(T su, T sv, T sw, T (&x)[5]) {
 template <int I, typename T>
 HD void slope_dir(T K, T irho, T U, T V, T W, T th, T it, const T (&dW)[5], T (&a)[5], T (&R)[5]) {
   const T hK3 = T(0.5) * (K + T(3)) * th;
-  const T c5 = T(2) / ((K + T(3)) * th * th);
+  const T c5 = T(2) * it * it * rcp(K + T(3));
   const T hK5t = T(0.5) * (K + T(5)) * th;
   const T b1 = dW[0] * irho, b2 = dW[1] * irho, b3 = dW[2] * irho, b4 = dW[3] * irho, b5 = dW[4] * irho;
   // b_c = T(-s) b
@@ -175,7 +213,7 @@ HD void slope_dir(T K, T irho, T U, T V, T W, T th, T it, const T (&dW)[5], T (&
 template <typename T>
 HD void temporal_slope(T K, T th, T it, const T (&R)[5], T (&A)[5]) {
   const T hK3 = T(0.5) * (K + T(3)) * th;
-  const T c5 = T(2) / ((K + T(3)) * th * th);
+  const T c5 = T(2) * it * it * rcp(K + T(3));
   const T r1 = -R[0];
   A[4] = c5 * (-R[4] - hK3 * r1);
   A[0] = r1 - hK3 * A[4];
@@ -206,26 +244,26 @@ struct GpFlux {
     dt = dt_;
     idt = idt_;
     const T isqpi = T(0.56418958354775628694807945156077);  // 1/sqrt(pi)
-    const T k3 = T(4) / (K + T(3));
+    const T k3 = T(4) * rcp(K + T(3));
     rl = WL[0];
-    irl = T(1) / rl;
+    irl = rcp(rl);
     Ul = WL[1] * irl;
     Vl = WL[2] * irl;
     Wl = WL[3] * irl;
     // theta = 1/(2 lambda) = 2 (rhoE - rho|U|^2/2) / ((K+3) rho)   (A.1)
     thl = T(0.5) * k3 * (WL[4] * irl - T(0.5) * (Ul * Ul + Vl * Vl + Wl * Wl));
     rr = WR[0];
-    irr = T(1) / rr;
+    irr = rcp(rr);
     Ur = WR[1] * irr;
     Vr = WR[2] * irr;
     Wr = WR[3] * irr;
     thr = T(0.5) * k3 * (WR[4] * irr - T(0.5) * (Ur * Ur + Vr * Vr + Wr * Wr));
     // half-space seeds (A.2): sqrt(lambda) = sqrt(1/(2 theta))
-    const T sl = m_sqrt(T(0.5) / thl), sr = m_sqrt(T(0.5) / thr);
+    const T sl = m_sqrt(T(0.5) * rcp(thl)), sr = m_sqrt(T(0.5) * rcp(thr));
     hl0 = T(0.5) * m_erfc(-sl * Ul);
-    hl1 = Ul * hl0 + T(0.5) * isqpi * m_exp(-sl * sl * Ul * Ul) / sl;
+    hl1 = Ul * hl0 + T(0.5) * isqpi * m_exp(-sl * sl * Ul * Ul) * rcp(sl);
     hr0 = T(0.5) * m_erfc(sr * Ur);
-    hr1 = Ur * hr0 - T(0.5) * isqpi * m_exp(-sr * sr * Ur * Ur) / sr;
+    hr1 = Ur * hr0 - T(0.5) * isqpi * m_exp(-sr * sr * Ur * Ur) * rcp(sr);
     // Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
     const T hl2 = Ul * hl1 + thl * hl0, hr2 = Ur * hr1 + thr * hr0;
     const T q0 = rl * hl0 + rr * hr0;
@@ -235,16 +273,16 @@ struct GpFlux {
     const T q4 = T(0.5) * (rl * (hl2 + hl0 * (Vl * Vl + Wl * Wl + (K + T(2)) * thl)) +
                            rr * (hr2 + hr0 * (Vr * Vr + Wr * Wr + (K + T(2)) * thr)));
     r0 = q0;
-    ir0 = T(1) / r0;
+    ir0 = rcp(r0);
     U0 = q1 * ir0;
     V0 = q2 * ir0;
     W0 = q3 * ir0;
     th0 = T(0.5) * k3 * (q4 * ir0 - T(0.5) * (U0 * U0 + V0 * V0 + W0 * W0));
     // tau = mu(T0)/p0 with T0 = theta0, p0 = rho0 theta0 (O-9)
     const T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
-    tau = mu * ir0 / th0;
+    tau = qdiv(mu * ir0, th0);
     // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
-    h = m_exp(-T(0.5) * dt / tau);
+    h = tau > T(0) ? m_exp(-T(0.5) * dt * rcp(tau)) : T(0);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       F[k] = T(0);
@@ -301,7 +339,7 @@ struct GpFlux {
   // X = U0 R + sum_i (s_i Q_x(a_i) + P_xi(a_i)) with P_xi(a) = <c_x c_i (a.psi) psi>.
   template <class Load>
   HD void add_equilibrium(Load&& load) {
-    const T th = th0, it = T(1) / th0;
+    const T th = th0, it = rcp(th0);
     const T hK3 = T(0.5) * (K + T(3)) * th;
     const T hK5t = T(0.5) * (K + T(5)) * th;
     const T t2 = th * th;
@@ -353,7 +391,7 @@ struct GpFlux {
   HD void add_side(Load&& load) {
     const T rho = SIDE > 0 ? rl : rr, irho = SIDE > 0 ? irl : irr;
     const T U = SIDE > 0 ? Ul : Ur, V = SIDE > 0 ? Vl : Vr, W = SIDE > 0 ? Wl : Wr;
-    const T th = SIDE > 0 ? thl : thr, it = T(1) / th;
+    const T th = SIDE > 0 ? thl : thr, it = rcp(th);
     // half-space u-moments t_0..t_6 (A.2 recursion)
     T t[7];
     t[0] = SIDE > 0 ? hl0 : hr0;
