@@ -122,10 +122,12 @@ int hgks_make_halo_plan(int32_t nx, int32_t ny, int32_t nz_local, int32_t rank, 
 
 /* ---- instrumentation (bench.py roofline / launch accounting) ----------------------------- */
 
-/* Kernel classes timed with CUDA events when profiling is enabled. */
+/* Kernel classes timed with CUDA events when profiling is enabled (FLUX_*: the fused
+ * tangential-reconstruction + Gauss-point flux sweep of one direction; RECON: the normal
+ * reconstruction sweeps of all three directions). */
 typedef enum {
   HGKS_K_FLUX_X = 0, HGKS_K_FLUX_Y = 1, HGKS_K_FLUX_Z = 2, HGKS_K_UPDATE = 3,
-  HGKS_K_GHOST = 4, HGKS_K_HALO = 5, HGKS_K_DT = 6, HGKS_K_COUNT = 7
+  HGKS_K_GHOST = 4, HGKS_K_HALO = 5, HGKS_K_DT = 6, HGKS_K_RECON = 7, HGKS_K_COUNT = 8
 } hgks_kernel_class;
 
 /* enable != 0: bracket every launch of each class with CUDA events on the compute stream.

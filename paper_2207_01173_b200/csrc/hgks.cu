@@ -48,6 +48,8 @@ struct hgks_ctx {
   void* Q[2] = {nullptr, nullptr};
   void* Qs = nullptr;
   void* F[3] = {nullptr, nullptr, nullptr};
+  void* FF = nullptr;       // face fields of one direction (recon_kernel output), reused per direction
+  size_t ff_elems = 0;
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;    // pinned
@@ -184,25 +186,36 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     attr_done[pi][STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  T* ff = (T*)c->FF;
+  auto recon_blocks = [&](int n1, int n2) { return (int)((5LL * (n1 + 4) * (n2 + 4) + 127) / 128); };
   {  // x faces: t1 = y, t2 = z
-    dim3 grid((ny + TT1 - 1) / TT1, (nz + TT2 - 1) / TT2, nx + 1);
+    prof_begin(c, HGKS_K_RECON);
+    recon_kernel<T, 0><<<recon_blocks(ny, nz), 128, 0, c->s>>>(q, ff, g, c->ctl);
+    prof_end(c, HGKS_K_RECON);
     prof_begin(c, HGKS_K_FLUX_X);
-    flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[0], g, gas, c->ctl);
+    dim3 grid((ny + TT1 - 1) / TT1, (nz + TT2 - 1) / TT2, nx + 1);
+    flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
     prof_end(c, HGKS_K_FLUX_X);
   }
   {  // y faces: t1 = z, t2 = x
-    dim3 grid((nz + TT1 - 1) / TT1, (nx + TT2 - 1) / TT2, ny + 1);
+    prof_begin(c, HGKS_K_RECON);
+    recon_kernel<T, 1><<<recon_blocks(nz, nx), 128, 0, c->s>>>(q, ff, g, c->ctl);
+    prof_end(c, HGKS_K_RECON);
     prof_begin(c, HGKS_K_FLUX_Y);
-    flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[1], g, gas, c->ctl);
+    dim3 grid((nz + TT1 - 1) / TT1, (nx + TT2 - 1) / TT2, ny + 1);
+    flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
     prof_end(c, HGKS_K_FLUX_Y);
   }
   {  // z faces: t1 = x, t2 = y
-    dim3 grid((nx + TT1 - 1) / TT1, (ny + TT2 - 1) / TT2, nz + 1);
+    prof_begin(c, HGKS_K_RECON);
+    recon_kernel<T, 2><<<recon_blocks(nx, ny), 128, 0, c->s>>>(q, ff, g, c->ctl);
+    prof_end(c, HGKS_K_RECON);
     prof_begin(c, HGKS_K_FLUX_Z);
-    flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(q, (T*)c->F[2], g, gas, c->ctl);
+    dim3 grid((nx + TT1 - 1) / TT1, (ny + TT2 - 1) / TT2, nz + 1);
+    flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
     prof_end(c, HGKS_K_FLUX_Z);
   }
-  c->total_launches += 3;
+  c->total_launches += 6;
   CUDA_TRY(c, cudaGetLastError());
   return HGKS_OK;
 }
@@ -350,6 +363,14 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   for (int b = 0; b < 2; ++b) ok = ok && cudaMalloc(&c->Q[b], c->qelems * c->esz) == cudaSuccess;
   ok = ok && cudaMalloc(&c->Qs, c->qelems * c->esz) == cudaSuccess;
   for (int d = 0; d < 3; ++d) ok = ok && cudaMalloc(&c->F[d], 10 * c->nface[d] * c->esz) == cudaSuccess;
+  // face-field buffer: 30 values per face-line, lines include the +-2 tangential halo
+  c->ff_elems = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int n3[3] = {c->n[0], c->n[1], c->nzl};
+    const size_t e = 30ull * (n3[d] + 1) * (n3[(d + 1) % 3] + 4) * (n3[(d + 2) % 3] + 4);
+    if (e > c->ff_elems) c->ff_elems = e;
+  }
+  ok = ok && cudaMalloc(&c->FF, c->ff_elems * c->esz) == cudaSuccess;
   ok = ok && cudaMalloc(&c->stage64, 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double)) == cudaSuccess;
   ok = ok && cudaMalloc(&c->ctl, sizeof(Ctl)) == cudaSuccess;
   ok = ok && cudaMallocHost(&c->ctl_host, sizeof(Ctl)) == cudaSuccess;
@@ -504,6 +525,7 @@ int hgks_destroy(hgks_ctx* c) {
   for (int b = 0; b < 2; ++b) cudaFree(c->Q[b]);
   cudaFree(c->Qs);
   for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
+  cudaFree(c->FF);
   cudaFree(c->stage64);
   cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);

@@ -64,8 +64,89 @@ constexpr size_t flux_smem_bytes() {
   return sizeof(T) * (6 * 5 * SA_C + TL2 * 5 * SB_RC);
 }
 
+// ---- normal reconstruction (A2): face fields of every face-line of one direction -------------
+// Face-field array of direction DIR (elements of T): ff[field][comp][fn][line], fields
+//   0 Ql, 1 Qr, 2 dQl/dn, 3 dQr/dn, 4 C, 5 D   (normal_fields, O-3 / O-6)
+// for faces fn = 0..n_DIR (face fn between cells fn-1 and fn) and tangential lines
+// (t1, t2) in [-2, n_t1+2) x [-2, n_t2+2) (the +-2 halo the tangential stencils need), line index
+// with the x-most tangent fastest: DIR 0 (t1 = y, t2 = z) and DIR 2 (t1 = x, t2 = y): t1 fastest;
+// DIR 1 (t1 = z, t2 = x): t2 fastest.
+template <typename T, int DIR>
+struct FFLayout {
+  int n1, n2, nf;   // tangential cells, faces along the normal
+  long long nl;     // lines per face plane
+  __device__ __forceinline__ long long line(int t1, int t2) const {
+    return DIR == 1 ? (long long)(t1 + 2) * (n2 + 4) + (t2 + 2) : (long long)(t2 + 2) * (n1 + 4) + (t1 + 2);
+  }
+  __device__ __forceinline__ long long at(int f, int c, int fn, long long l) const {
+    return ((long long)(f * 5 + c) * nf + fn) * nl + l;
+  }
+};
+
+template <typename T, int DIR>
+__device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
+  constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;
+  FFLayout<T, DIR> L;
+  L.n1 = g.n[A1];
+  L.n2 = g.n[A2];
+  L.nf = g.n[DIR] + 1;
+  L.nl = (long long)(L.n1 + 4) * (L.n2 + 4);
+  return L;
+}
+
+// One thread per (line, component): marches along the normal with a 6-cell register ring, so
+// every cell's WENO edge pair is computed exactly once.
+template <typename T, int DIR>
+__global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
+                                                    const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;
+  const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= 5 * L.nl) return;
+  const int c = (int)(e / L.nl);
+  const long long l = e % L.nl;
+  int t1, t2;
+  if (DIR == 1) {
+    t1 = (int)(l / (L.n2 + 4)) - 2;
+    t2 = (int)(l % (L.n2 + 4)) - 2;
+  } else {
+    t2 = (int)(l / (L.n1 + 4)) - 2;
+    t1 = (int)(l % (L.n1 + 4)) - 2;
+  }
+  const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
+  const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
+  const long long s2 = (A2 == 0) ? 1 : (A2 == 1 ? g.px : g.plane);
+  const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 1 + DIR : (c == 2 ? 1 + A1 : 1 + A2)));
+  // cell -3 along the normal at (t1, t2)
+  const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + t1 * s1 + t2 * s2;
+  const T ih = g.ih[DIR];
+  T s0 = p[0], s1v = p[sN], s2v = p[2 * sN], s3 = p[3 * sN], s4 = p[4 * sN], s5;
+  T Ap, Bp;  // edges of cell fn-1
+  weno5z_cell(s0, s1v, s2v, s3, s4, Ap, Bp);  // cell -1 (stencil -3..1)
+  const int nf = L.nf;
+  for (int fn = 0; fn < nf; ++fn) {
+    s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; ring s0..s5 = Qbar_{fn-3..fn+2}
+    T Ac, Bc;
+    weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn (stencil fn-2..fn+2)
+    ff[L.at(0, c, fn, l)] = Bp;
+    ff[L.at(1, c, fn, l)] = Ac;
+    ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
+    ff[L.at(3, c, fn, l)] = (T(-4) * Ac - T(2) * Bc + T(6) * s3) * ih;
+    ff[L.at(4, c, fn, l)] = (-s1v + T(7) * s2v + T(7) * s3 - s4) * T(1.0 / 12.0);
+    ff[L.at(5, c, fn, l)] = (s1v - T(15) * s2v + T(15) * s3 - s4) * (T(1.0 / 12.0) * ih);
+    s0 = s1v;
+    s1v = s2v;
+    s2v = s3;
+    s3 = s4;
+    s4 = s5;
+    Ap = Ac;
+    Bp = Bc;
+  }
+}
+
 // Fused flux sweep of one direction for one tile of TT1 x TT2 faces at normal face index fn:
-//   A  normal reconstruction (A2) of the (TT1+4) x (TT2+4) lines -> sA[field][comp][l2][l1]
+//   A  copy of the face fields (A2, from recon_kernel) of the (TT1+4) x (TT2+4) lines -> sA
 //   B  t1 pass (A3): values at the two t1 Gauss abscissae of all 6 fields and t1-derivatives of
 //      Ql, Qr, C on every row -> sB[l2][comp][slot][m][a]
 //   C  one thread per Gauss point: t2 pass, loaded lazily one derivative direction at a time,
@@ -74,7 +155,7 @@ constexpr size_t flux_smem_bytes() {
 // warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
 template <typename T, int DIR, int STAGE>
 __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
-    flux_kernel(const T* __restrict__ q, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
+    flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -83,66 +164,79 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
 
   const int n1 = g.n[A1], n2 = g.n[A2];
   const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2, fn = blockIdx.z;  // face fn: cells fn-1 | fn
-  const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
-  const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
-  const long long s2 = (A2 == 0) ? 1 : (A2 == 1 ? g.px : g.plane);
-  const T ihN = g.ih[DIR];
-
-  // ---- phase A: normal reconstruction of TL1 x TL2 lines, 5 components --------------------
-  for (int w = threadIdx.x; w < TL1 * TL2 * 5; w += NTHREADS_FLUX) {
-    const int l1 = w % TL1;
-    const int rest = w / TL1;
-    const int l2 = rest % TL2;
-    const int c = rest / TL2;
-    int g1 = t10 + l1 - 2, g2 = t20 + l2 - 2;
-    g1 = min(max(g1, -3), n1 + 2);  // ragged tiles: clamp (values unused)
-    g2 = min(max(g2, -3), n2 + 2);
-    const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 1 + DIR : (c == 2 ? 1 + A1 : 1 + A2)));
-    // cell (fn - 3) along the normal, (g1, g2) tangentially; interior index origin at +3 ghosts
-    const long long base =
-        3LL * (g.plane + g.px + 1) + (long long)gv * g.vs + (long long)(fn - 3) * sN + g1 * s1 + g2 * s2;
-    T s[6];
+  // ---- phase A: tile of face fields (6 x 5 x TL1 x TL2) from the reconstruction array -------
+  // asynchronous global->shared copies (cp.async / LDGSTS): each thread owns one tile line
+  // (l1, l2) and copies its 30 (field, component) values, all in flight at once
+  {
+    const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
+    const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sA);
+    constexpr int NLINE = TL1 * TL2;
+    constexpr int NPASS = (NLINE + NTHREADS_FLUX - 1) / NTHREADS_FLUX;
 #pragma unroll
-    for (int r = 0; r < 6; ++r) s[r] = q[base + r * sN];
-    T f[6];
-    normal_fields(s, ihN, f);
+    for (int pass = 0; pass < NPASS; ++pass) {
+      const int j = threadIdx.x + pass * NTHREADS_FLUX;
+      if (j < NLINE) {
+        int l1, l2;
+        if (DIR == 1) {  // t2 is the contiguous axis of the array
+          l2 = j % TL2;
+          l1 = j / TL2;
+        } else {
+          l1 = j % TL1;
+          l2 = j / TL1;
+        }
+        const int t1 = min(t10 + l1 - 2, n1 + 1), t2 = min(t20 + l2 - 2, n2 + 1);  // ragged tiles: clamp
+        const T* src = ff + (long long)fn * L.nl + L.line(t1, t2);
+        unsigned dst = sbase + (unsigned)((l2 * TL1 + l1) * sizeof(T));
 #pragma unroll
-    for (int ff = 0; ff < 6; ++ff) sA[(ff * 5 + c) * SA_C + l2 * TL1 + l1] = f[ff];
+        for (int fc = 0; fc < 30; ++fc) {
+          if (sizeof(T) == 8)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+          else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+          src += fstride;
+          dst += SA_C * sizeof(T);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
 
   // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
-  // Gauss point m = 1 uses the mirrored weights: wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
-  for (int w = threadIdx.x; w < TT1 * 5 * TL2 * 2; w += NTHREADS_FLUX) {
+  // One item = (a, c, l2) computes both Gauss abscissae m = 0, 1 from the same 30 loads: point
+  // m = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
+  for (int w = threadIdx.x; w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
     const int c = (w / TT1) % 5;
-    const int rest = w / (TT1 * 5);
-    const int l2 = rest % TL2;
-    const int m = rest / TL2;
-    T out[NB];
+    const int l2 = w / (TT1 * 5);
+    T o0[NB], o1[NB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) out[k] = T(0);
+    for (int k = 0; k < NB; ++k) {
+      o0[k] = T(0);
+      o1[k] = T(0);
+    }
     const T* src = sA + c * SA_C + l2 * TL1 + a;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const int rr = m ? 4 - r : r;
-      const T wv = T(kWV0(r)), wd = T(kWD0(r));
+      const T wv0 = T(kWV0(r)), wd0 = T(kWD0(r));          // m = 0 weights of tap r
+      const T wv1 = T(kWV0(4 - r)), wd1 = -T(kWD0(4 - r));  // m = 1 weights of tap r
 #pragma unroll
       for (int ff = 0; ff < 6; ++ff) {
-        const T x = src[ff * 5 * SA_C + rr];
-        out[ff] += wv * x;
-        if (ff == 0) out[6] += wd * x;
-        if (ff == 1) out[7] += wd * x;
-        if (ff == 4) out[8] += wd * x;
+        const T x = src[ff * 5 * SA_C + r];
+        o0[ff] += wv0 * x;
+        o1[ff] += wv1 * x;
+        if (ff == 0) { o0[6] += wd0 * x; o1[6] += wd1 * x; }
+        if (ff == 1) { o0[7] += wd0 * x; o1[7] += wd1 * x; }
+        if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
       }
     }
-    const T sg = m ? T(-1) : T(1);
-    out[6] *= sg;
-    out[7] *= sg;
-    out[8] *= sg;
-    T* dst = sB + (l2 * 5 + c) * SB_RC + m * TT1 + a;
+    T* dst = sB + (l2 * 5 + c) * SB_RC + a;
 #pragma unroll
-    for (int k = 0; k < NB; ++k) dst[k * SB_K] = out[k];
+    for (int k = 0; k < NB; ++k) {
+      dst[k * SB_K] = o0[k];
+      dst[k * SB_K + TT1] = o1[k];
+    }
   }
   __syncthreads();
 

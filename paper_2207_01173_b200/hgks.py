@@ -23,7 +23,7 @@ HGKS_OK, HGKS_EINVAL, HGKS_ECUDA, HGKS_ENCCL, HGKS_ESTATE, HGKS_ENOMEM = 0, -1, 
 HGKS_FP64, HGKS_FP32 = 0, 1
 HGKS_PERIODIC, HGKS_WALL_ISOTHERMAL = 0, 1
 HGKS_MU_CONST, HGKS_MU_POWER = 0, 1
-KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt")
+KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt", "recon")
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",

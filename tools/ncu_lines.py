@@ -64,7 +64,7 @@ def main(rep, lib, ksub, kidx=0, mangled_sub=None):
         by_op[opc][0] += s
         by_op[opc][1] += ins
     print("total samples", tot)
-    for k, v in sorted(by_line.items(), key=lambda x: -x[1][0])[:45]:
+    for k, v in sorted(by_line.items(), key=lambda x: -x[1][0])[:int(__import__("os").environ.get("TOPN","45"))]:
         print(f"{v[0] / tot * 100:6.2f}%  inst={v[1]:>12d}  {k}")
     print("-- by opcode")
     for k, v in sorted(by_op.items(), key=lambda x: -x[1][0])[:20]:
