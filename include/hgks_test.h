@@ -27,6 +27,11 @@ int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, do
  * P:355-358) written to host arrays L, dL in the set_state layout.  Used for per-stage parity. */
 int hgks_test_operator(hgks_ctx* c, double dt, double* L, double* dL);
 
+/* Face-flux array of direction dir (0 x, 1 y, 2 z) left by the last flux sweep (e.g. after
+ * hgks_test_operator): out[10][nfaces] fp64 with components 0..4 = F^n, 5..9 = d_t F^n per unit
+ * area, faces in natural [z][y][x] order with the normal extent n_dir + 1.  Synchronises. */
+int hgks_test_face_flux(hgks_ctx* c, int dir, double* out);
+
 #ifdef __cplusplus
 }
 #endif

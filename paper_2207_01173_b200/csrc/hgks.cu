@@ -48,8 +48,10 @@ struct hgks_ctx {
   void* Q[2] = {nullptr, nullptr};
   void* Qs = nullptr;
   void* F[3] = {nullptr, nullptr, nullptr};
-  void* FF = nullptr;       // face fields of one direction (recon_kernel output), reused per direction
+  void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
+  cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
+  cudaEvent_t ev_in = nullptr, ev_rec[3] = {}, ev_flux[3] = {};
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;    // pinned
@@ -88,17 +90,17 @@ static int fail(hgks_ctx* c, int code, const char* fmt, ...) {
   } while (0)
 
 // ---- instrumentation ------------------------------------------------------------------------
-static void prof_begin(hgks_ctx* c, int cls) {
+static void prof_begin(hgks_ctx* c, int cls, cudaStream_t st = nullptr) {
   c->prof.launches[cls] += 1;
   if (!c->prof.on || c->prof.nev >= 4096) return;
   int k = c->prof.nev;
   c->prof.cls[k] = cls;
-  cudaEventRecord(c->prof.ev[2 * k], c->s);
+  cudaEventRecord(c->prof.ev[2 * k], st ? st : c->s);
 }
-static void prof_end(hgks_ctx* c, int cls) {
+static void prof_end(hgks_ctx* c, int cls, cudaStream_t st = nullptr) {
   (void)cls;
   if (!c->prof.on || c->prof.nev >= 4096) return;
-  cudaEventRecord(c->prof.ev[2 * c->prof.nev + 1], c->s);
+  cudaEventRecord(c->prof.ev[2 * c->prof.nev + 1], st ? st : c->s);
   c->prof.nev += 1;
 }
 static void prof_flush(hgks_ctx* c) {  // fold recorded events into ms[] (caller synchronised)
@@ -186,35 +188,42 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     attr_done[pi][STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  T* ff = (T*)c->FF;
   auto recon_blocks = [&](int n1, int n2) { return (int)((5LL * (n1 + 4) * (n2 + 4) + 127) / 128); };
-  {  // x faces: t1 = y, t2 = z
-    prof_begin(c, HGKS_K_RECON);
-    recon_kernel<T, 0><<<recon_blocks(ny, nz), 128, 0, c->s>>>(q, ff, g, c->ctl);
-    prof_end(c, HGKS_K_RECON);
-    prof_begin(c, HGKS_K_FLUX_X);
-    dim3 grid((ny + TT1 - 1) / TT1, (nz + TT2 - 1) / TT2, nx + 1);
-    flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
-    prof_end(c, HGKS_K_FLUX_X);
-  }
-  {  // y faces: t1 = z, t2 = x
-    prof_begin(c, HGKS_K_RECON);
-    recon_kernel<T, 1><<<recon_blocks(nz, nx), 128, 0, c->s>>>(q, ff, g, c->ctl);
-    prof_end(c, HGKS_K_RECON);
-    prof_begin(c, HGKS_K_FLUX_Y);
-    dim3 grid((nz + TT1 - 1) / TT1, (nx + TT2 - 1) / TT2, ny + 1);
-    flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
-    prof_end(c, HGKS_K_FLUX_Y);
-  }
-  {  // z faces: t1 = x, t2 = y
-    prof_begin(c, HGKS_K_RECON);
-    recon_kernel<T, 2><<<recon_blocks(nx, ny), 128, 0, c->s>>>(q, ff, g, c->ctl);
-    prof_end(c, HGKS_K_RECON);
-    prof_begin(c, HGKS_K_FLUX_Z);
-    dim3 grid((nx + TT1 - 1) / TT1, (ny + TT2 - 1) / TT2, nz + 1);
-    flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
-    prof_end(c, HGKS_K_FLUX_Z);
-  }
+  // Two streams: the reconstruction sweep of direction d+1 (memory-bound) runs on s2 while the
+  // flux sweep of direction d (FP64-bound) runs on s.  FF[d % 2] is written by recon d and read
+  // by flux d; recon d+2 waits for flux d before reusing the buffer.
+  CUDA_TRY(c, cudaEventRecord(c->ev_in, c->s));  // stage input ready (ghosts filled)
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_in, 0));
+  const int n3[3] = {nx, ny, nz};
+  auto recon = [&](int d) -> int {
+    T* ff = (T*)c->FF[d & 1];
+    const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
+    prof_begin(c, HGKS_K_RECON, c->s2);
+    if (d == 0) recon_kernel<T, 0><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
+    if (d == 1) recon_kernel<T, 1><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
+    if (d == 2) recon_kernel<T, 2><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
+    prof_end(c, HGKS_K_RECON, c->s2);
+    CUDA_TRY(c, cudaEventRecord(c->ev_rec[d], c->s2));
+    return HGKS_OK;
+  };
+  auto flux = [&](int d) -> int {
+    T* ff = (T*)c->FF[d & 1];
+    const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
+    dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, n3[d] + 1);
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
+    prof_begin(c, HGKS_K_FLUX_X + d);
+    if (d == 0) flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
+    if (d == 1) flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
+    if (d == 2) flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
+    prof_end(c, HGKS_K_FLUX_X + d);
+    CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
+    return HGKS_OK;
+  };
+  // enqueue order matters: an event must be recorded before a wait on it is enqueued
+  int rc;
+  if ((rc = recon(0)) || (rc = recon(1)) || (rc = flux(0))) return rc;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_flux[0], 0));  // FF[0] free again
+  if ((rc = recon(2)) || (rc = flux(1)) || (rc = flux(2))) return rc;
   c->total_launches += 6;
   CUDA_TRY(c, cudaGetLastError());
   return HGKS_OK;
@@ -370,7 +379,13 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     const size_t e = 30ull * (n3[d] + 1) * (n3[(d + 1) % 3] + 4) * (n3[(d + 2) % 3] + 4);
     if (e > c->ff_elems) c->ff_elems = e;
   }
-  ok = ok && cudaMalloc(&c->FF, c->ff_elems * c->esz) == cudaSuccess;
+  for (int b = 0; b < 2; ++b) ok = ok && cudaMalloc(&c->FF[b], c->ff_elems * c->esz) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess;
+  for (int d = 0; d < 3; ++d) {
+    ok = ok && cudaEventCreateWithFlags(&c->ev_rec[d], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_flux[d], cudaEventDisableTiming) == cudaSuccess;
+  }
   ok = ok && cudaMalloc(&c->stage64, 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double)) == cudaSuccess;
   ok = ok && cudaMalloc(&c->ctl, sizeof(Ctl)) == cudaSuccess;
   ok = ok && cudaMallocHost(&c->ctl_host, sizeof(Ctl)) == cudaSuccess;
@@ -525,7 +540,13 @@ int hgks_destroy(hgks_ctx* c) {
   for (int b = 0; b < 2; ++b) cudaFree(c->Q[b]);
   cudaFree(c->Qs);
   for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
-  cudaFree(c->FF);
+  for (int b = 0; b < 2; ++b) cudaFree(c->FF[b]);
+  if (c->s2) cudaStreamDestroy(c->s2);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  for (int d = 0; d < 3; ++d) {
+    if (c->ev_rec[d]) cudaEventDestroy(c->ev_rec[d]);
+    if (c->ev_flux[d]) cudaEventDestroy(c->ev_flux[d]);
+  }
   cudaFree(c->stage64);
   cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);
@@ -622,6 +643,22 @@ static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
 }
 
 extern "C" {
+
+int hgks_test_face_flux(hgks_ctx* c, int dir, double* out) {
+  if (!c || !out || dir < 0 || dir > 2) return fail(c, HGKS_EINVAL, "hgks_test_face_flux: bad arguments");
+  const size_t n = 10 * c->nface[dir];
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  if (c->fp32) {
+    float* h = (float*)malloc(n * sizeof(float));
+    cudaError_t e = cudaMemcpy(h, c->F[dir], n * sizeof(float), cudaMemcpyDeviceToHost);
+    for (size_t k = 0; k < n; ++k) out[k] = h[k];
+    free(h);
+    if (e != cudaSuccess) return fail(c, HGKS_ECUDA, "hgks_test_face_flux: %s", cudaGetErrorString(e));
+  } else {
+    CUDA_TRY(c, cudaMemcpy(out, c->F[dir], n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return HGKS_OK;
+}
 
 int hgks_test_operator(hgks_ctx* c, double dt, double* L, double* dL) {
   if (!c || !L || !dL || !(dt > 0)) return fail(c, HGKS_EINVAL, "hgks_test_operator: bad arguments");

@@ -121,21 +121,23 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   // cell -3 along the normal at (t1, t2)
   const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + t1 * s1 + t2 * s2;
   const T ih = g.ih[DIR];
-  T s0 = p[0], s1v = p[sN], s2v = p[2 * sN], s3 = p[3 * sN], s4 = p[4 * sN], s5;
-  T Ap, Bp;  // edges of cell fn-1
-  weno5z_cell(s0, s1v, s2v, s3, s4, Ap, Bp);  // cell -1 (stencil -3..1)
+  // every cell's WENO pair is evaluated at the same call site (the loop body), so all faces see
+  // bitwise-identical arithmetic (uniform flow stays exactly uniform, O-P1)
+  T s1v = p[0], s2v = p[sN], s3 = p[2 * sN], s4 = p[3 * sN], s5;
+  T Ap = T(0), Bp = T(0);  // edges of cell fn-1
   const int nf = L.nf;
-  for (int fn = 0; fn < nf; ++fn) {
-    s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; ring s0..s5 = Qbar_{fn-3..fn+2}
+  for (int fn = -1; fn < nf; ++fn) {
+    s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
     T Ac, Bc;
-    weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn (stencil fn-2..fn+2)
-    ff[L.at(0, c, fn, l)] = Bp;
-    ff[L.at(1, c, fn, l)] = Ac;
-    ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
-    ff[L.at(3, c, fn, l)] = (T(-4) * Ac - T(2) * Bc + T(6) * s3) * ih;
-    ff[L.at(4, c, fn, l)] = (-s1v + T(7) * s2v + T(7) * s3 - s4) * T(1.0 / 12.0);
-    ff[L.at(5, c, fn, l)] = (s1v - T(15) * s2v + T(15) * s3 - s4) * (T(1.0 / 12.0) * ih);
-    s0 = s1v;
+    weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
+    if (fn >= 0) {
+      ff[L.at(0, c, fn, l)] = Bp;
+      ff[L.at(1, c, fn, l)] = Ac;
+      ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
+      ff[L.at(3, c, fn, l)] = (T(-4) * Ac - T(2) * Bc + T(6) * s3) * ih;
+      ff[L.at(4, c, fn, l)] = (-s1v + T(7) * s2v + T(7) * s3 - s4) * T(1.0 / 12.0);
+      ff[L.at(5, c, fn, l)] = (s1v - T(15) * s2v + T(15) * s3 - s4) * (T(1.0 / 12.0) * ih);
+    }
     s1v = s2v;
     s2v = s3;
     s3 = s4;

@@ -27,7 +27,7 @@ KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt",
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_test_gp_flux", "hgks_test_operator")
+            "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
 
 
 class HgksError(RuntimeError):
@@ -80,6 +80,7 @@ def lib():
         L.hgks_test_gp_flux.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
                                         C.c_double, C.c_double, _dp, C.c_int64, _dp]
         L.hgks_test_operator.argtypes = [vp, C.c_double, _dp, _dp]
+        L.hgks_test_face_flux.argtypes = [vp, C.c_int, _dp]
         _lib = L
     return _lib
 
@@ -204,6 +205,15 @@ def hgks_test_operator(ctx, dt: float, shape):
     L, dL = np.zeros(shape), np.zeros(shape)
     _check(lib().hgks_test_operator(ctx, dt, L.ctypes.data_as(_dp), dL.ctypes.data_as(_dp)), ctx)
     return L, dL
+
+
+def hgks_test_face_flux(ctx, d: int, n) -> np.ndarray:
+    """[10][nz'][ny'][nx'] face fluxes of direction d after the last sweep (n = local (nx,ny,nz))."""
+    dims = [n[2], n[1], n[0]]
+    dims[2 - d] += 1
+    out = np.zeros((10, *dims))
+    _check(lib().hgks_test_face_flux(ctx, d, out.ctypes.data_as(_dp)), ctx)
+    return out
 
 
 class Solver:

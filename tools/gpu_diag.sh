@@ -1,0 +1,1 @@
+python tools/diag_uniform.py; timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
