@@ -153,6 +153,7 @@ def main():
     ap.add_argument("--n", type=int, default=256, help="TGV grid n^3 (BASELINE config 3: 256)")
     ap.add_argument("--weak", action="store_true", help="weak scaling: n x n x (n/8 * N) per job")
     ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--only-fp32", action="store_true", help="profiling aid: run only the fp32 leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-planes", type=int, default=4)
@@ -208,6 +209,8 @@ def main():
     for prec_name, prec in (("fp64", H.HGKS_FP64), ("fp32", H.HGKS_FP32)):
         if prec_name == "fp32" and args.no_fp32:
             continue
+        if prec_name == "fp64" and args.only_fp32:
+            continue
         s = make_solver(prec)
         q = local_field(s)
         qd = torch.from_numpy(q).cuda()
@@ -254,7 +257,7 @@ def main():
         torch.cuda.empty_cache()
         results[prec_name] = res
 
-    if rank != 0:
+    if rank != 0 or args.only_fp32:
         if ws > 1:
             dist.destroy_process_group()
         return
