@@ -214,6 +214,29 @@ void or_time_integrals(double T, double tau, double g[6]) {
   g[5] = -tau * tau * (1.0 - e);
 }
 
+/* ------------------------------------------------------------------------------------------
+ * Axis geometry (P:219-223 uniform; P:945-956 tanh-stretched channel, O-18)
+ * ---------------------------------------------------------------------------------------- */
+double or_axis_face(const or_grid* gr, int d, int j) {
+  if (gr->stretch[d] == 0) return gr->lo[d] + j * gr->dx[d];
+  double b = gr->stretch_b[d], s = (double)j / gr->n[d];
+  return 0.5 * (gr->lo[d] + gr->hi[d]) + 0.5 * (gr->hi[d] - gr->lo[d]) * tanh(b * (2.0 * s - 1.0)) / tanh(b);
+}
+
+/* J = d zeta / dx with zeta the cell-index coordinate (x(zeta) = or_axis_face at integer zeta) */
+double or_axis_metric(const or_grid* gr, int d, double zeta) {
+  if (gr->stretch[d] == 0) return 1.0 / gr->dx[d];
+  double b = gr->stretch_b[d], n = gr->n[d];
+  double ch = cosh(b * (2.0 * zeta / n - 1.0));
+  double dxdz = 0.5 * (gr->hi[d] - gr->lo[d]) / tanh(b) * b * (2.0 / n) / (ch * ch);
+  return 1.0 / dxdz;
+}
+
+static double cell_width(const or_grid* gr, int d, int j) {
+  if (gr->stretch[d] == 0) return gr->dx[d];
+  return or_axis_face(gr, d, j + 1) - or_axis_face(gr, d, j);
+}
+
 /* viscosity law (O-9) at temperature T = p/rho */
 static double mu_of(const or_gas* g, double T) {
   if (g->mu_law == 1) return g->mu_ref * pow(T / g->T_ref, g->omega);
@@ -310,6 +333,56 @@ int or_gp_flux(const or_gas* g, const double Wl[5], const double dWl[3][5], cons
     F[k] = (Ifull[k] * a22 - a12 * Ihalf[k]) / det;
     dF[k] = (a11 * Ihalf[k] - a21 * Ifull[k]) / det;
   }
+
+  /* Pr != 1 (reading O-12): add (1/Pr - 1) q to the energy flux, q the heat flux
+   * int (u - U0) (|u - U0|^2 + xi^2)/2 f dXi of the interface distribution of Eq. (6) relative to
+   * the interface equilibrium velocity U0, linearised in time like the flux.  With F = int u psi f
+   * and Wd = int psi f (density moments of the same six terms):
+   *   q = F5 - U0.F_m + |U0|^2 F1/2 - U0 (Wd5 - U0.Wd_m + |U0|^2 Wd1/2). */
+  if (g->prandtl != 1.0) {
+    double Dk[6][5];
+    mom_psi(&t0, 0, 0, 0, 0, tmp);
+    for (int k = 0; k < 5; ++k) Dk[0][k] = m0[0] * tmp[k];
+    mom_poly_psi(&t0, 1, 0, 0, ab[0], t1);
+    mom_poly_psi(&t0, 0, 1, 0, ab[1], t2);
+    mom_poly_psi(&t0, 0, 0, 1, ab[2], t3);
+    for (int k = 0; k < 5; ++k) Dk[1][k] = m0[0] * (t1[k] + t2[k] + t3[k]);
+    mom_poly_psi(&t0, 0, 0, 0, Ab, tmp);
+    for (int k = 0; k < 5; ++k) Dk[2][k] = m0[0] * tmp[k];
+    for (int k = 0; k < 5; ++k) Dk[3][k] = ml[0] * pl[k] + mr[0] * pr[k];
+    double d5l[5], d5r[5];
+    mom_poly_psi(&tl_pos, 1, 0, 0, al[0], t1);
+    mom_poly_psi(&tl_pos, 0, 1, 0, al[1], t2);
+    mom_poly_psi(&tl_pos, 0, 0, 1, al[2], t3);
+    for (int k = 0; k < 5; ++k) d5l[k] = t1[k] + t2[k] + t3[k];
+    mom_poly_psi(&tr_neg, 1, 0, 0, ar[0], t1);
+    mom_poly_psi(&tr_neg, 0, 1, 0, ar[1], t2);
+    mom_poly_psi(&tr_neg, 0, 0, 1, ar[2], t3);
+    for (int k = 0; k < 5; ++k) d5r[k] = t1[k] + t2[k] + t3[k];
+    for (int k = 0; k < 5; ++k) Dk[4][k] = ml[0] * d5l[k] + mr[0] * d5r[k];
+    double d6l[5], d6r[5];
+    mom_poly_psi(&tl_pos, 0, 0, 0, Al, d6l);
+    mom_poly_psi(&tr_neg, 0, 0, 0, Ar, d6r);
+    for (int k = 0; k < 5; ++k) Dk[5][k] = ml[0] * d6l[k] + mr[0] * d6r[k];
+    double Jf[5], Jh[5], Wn[5], dWn[5];
+    for (int k = 0; k < 5; ++k) {
+      Jf[k] = 0.0;
+      Jh[k] = 0.0;
+      for (int j = 0; j < 6; ++j) {
+        Jf[k] += gf[j] * Dk[j][k];
+        Jh[k] += gh[j] * Dk[j][k];
+      }
+      Wn[k] = (Jf[k] * a22 - a12 * Jh[k]) / det;
+      dWn[k] = (a11 * Jh[k] - a21 * Jf[k]) / det;
+    }
+    double U0 = m0[1], V0 = m0[2], W0 = m0[3], u2 = 0.5 * (U0 * U0 + V0 * V0 + W0 * W0);
+    double q = F[4] - (U0 * F[1] + V0 * F[2] + W0 * F[3]) + u2 * F[0] -
+               U0 * (Wn[4] - (U0 * Wn[1] + V0 * Wn[2] + W0 * Wn[3]) + u2 * Wn[0]);
+    double dq = dF[4] - (U0 * dF[1] + V0 * dF[2] + W0 * dF[3]) + u2 * dF[0] -
+                U0 * (dWn[4] - (U0 * dWn[1] + V0 * dWn[2] + W0 * dWn[3]) + u2 * dWn[0]);
+    F[4] += (1.0 / g->prandtl - 1.0) * q;
+    dF[4] += (1.0 / g->prandtl - 1.0) * dq;
+  }
   for (int k = 0; k < 5; ++k)
     if (!isfinite(F[k]) || !isfinite(dF[k])) return -1;
   return 0;
@@ -370,9 +443,9 @@ static void quartic_weights(double x, double wv[5], double wd[5]) {
 /* 2x2 Gauss-Legendre abscissae -+ sqrt(3)/6 of the unit cell width, weights 1/4 (O-8) */
 static double gauss_abscissa(int m) { return (m == 0 ? -1.0 : 1.0) * sqrt(3.0) / 6.0; }
 
-void or_face_gauss_points(const double cells[6][5][5][5], const double h[3], double Wl[4][5],
-                          double Wr[4][5], double dWl[4][3][5], double dWr[4][3][5],
-                          double dW0[4][3][5]) {
+void or_face_gauss_points(const double cells[6][5][5][5], double Jn, const double Jt1[2],
+                          const double Jt2[2], double Wl[4][5], double Wr[4][5], double dWl[4][3][5],
+                          double dWr[4][3][5], double dW0[4][3][5]) {
   /* normal pass on each of the 5x5 tangential lines: six face fields per component */
   double Ql[5][5][5], Qr[5][5][5], dQl[5][5][5], dQr[5][5][5], Cf[5][5][5], Df[5][5][5];
   for (int a = 0; a < 5; ++a)
@@ -384,10 +457,10 @@ void or_face_gauss_points(const double cells[6][5][5][5], const double h[3], dou
         double Aj = or_weno5z_left(&s[1]), Bj = or_weno5z_right(&s[1]), Mj = s[3];
         Ql[a][b][c] = Bi;                                        /* left state  = cell i right edge   */
         Qr[a][b][c] = Aj;                                        /* right state = cell i+1 left edge  */
-        dQl[a][b][c] = (2.0 * Ai + 4.0 * Bi - 6.0 * Mi) / h[0];  /* O-3 in-cell parabola slope       */
-        dQr[a][b][c] = (-4.0 * Aj - 2.0 * Bj + 6.0 * Mj) / h[0];
+        dQl[a][b][c] = (2.0 * Ai + 4.0 * Bi - 6.0 * Mi) * Jn;  /* O-3 in-cell parabola slope        */
+        dQr[a][b][c] = (-4.0 * Aj - 2.0 * Bj + 6.0 * Mj) * Jn;
         Cf[a][b][c] = (-s[1] + 7.0 * s[2] + 7.0 * s[3] - s[4]) / 12.0;        /* O-6 */
-        Df[a][b][c] = (s[1] - 15.0 * s[2] + 15.0 * s[3] - s[4]) / (12.0 * h[0]);
+        Df[a][b][c] = (s[1] - 15.0 * s[2] + 15.0 * s[3] - s[4]) / 12.0 * Jn;
       }
   /* tangential pass (O-4): tensor-product quartic weights at the 2x2 Gauss points */
   double wv[2][5], wd[2][5];
@@ -418,14 +491,14 @@ void or_face_gauss_points(const double cells[6][5][5][5], const double h[3], dou
         Wl[gp][c] = vQl;
         Wr[gp][c] = vQr;
         dWl[gp][0][c] = vdQl;
-        dWl[gp][1][c] = d1Ql / h[1];
-        dWl[gp][2][c] = d2Ql / h[2];
+        dWl[gp][1][c] = d1Ql * Jt1[m];
+        dWl[gp][2][c] = d2Ql * Jt2[n];
         dWr[gp][0][c] = vdQr;
-        dWr[gp][1][c] = d1Qr / h[1];
-        dWr[gp][2][c] = d2Qr / h[2];
+        dWr[gp][1][c] = d1Qr * Jt1[m];
+        dWr[gp][2][c] = d2Qr * Jt2[n];
         dW0[gp][0][c] = vD;
-        dW0[gp][1][c] = d1C / h[1];
-        dW0[gp][2][c] = d2C / h[2];
+        dW0[gp][1][c] = d1C * Jt1[m];
+        dW0[gp][2][c] = d2C * Jt2[n];
       }
     }
 }
@@ -445,15 +518,52 @@ static inline int wrap(int i, int n) {
   return r < 0 ? r + n : r;
 }
 
-void or_fill_ghosts_periodic(const or_grid* gr, double* q) {
-  int nx = gr->n[0], ny = gr->n[1], nz = gr->n[2];
+/* isothermal no-slip mirror (O-17): U_g = -U_m, T_g = 2 T_w - T_m, p_g = p_m, rho_g = p_g / T_g */
+static void wall_mirror(const or_gas* g, const double m[5], double gq[5]) {
+  double rho = m[0], U = m[1] / rho, V = m[2] / rho, W = m[3] / rho;
+  double p = (g->gamma - 1.0) * (m[4] - 0.5 * rho * (U * U + V * V + W * W));
+  double Tg = 2.0 * g->T_wall - p / rho;
+  double rg = p / Tg;
+  gq[0] = rg;
+  gq[1] = -rg * U;
+  gq[2] = -rg * V;
+  gq[3] = -rg * W;
+  gq[4] = p / (g->gamma - 1.0) + 0.5 * rg * (U * U + V * V + W * W);
+}
+
+void or_fill_ghosts(const or_gas* g, const or_grid* gr, double* q) {
+  int n[3] = {gr->n[0], gr->n[1], gr->n[2]};
+  /* 1. wall axes over the interior range of the other axes */
+  for (int d = 0; d < 3; ++d) {
+    if (gr->bc[d] != 1) continue;
+    int a1 = (d + 1) % 3, a2 = (d + 2) % 3;
+    for (int i2 = 0; i2 < n[a2]; ++i2)
+      for (int i1 = 0; i1 < n[a1]; ++i1)
+        for (int m = 0; m < OR_NG; ++m)
+          for (int side = 0; side < 2; ++side) {
+            int pm[3], pg[3];
+            pm[a1] = pg[a1] = i1;
+            pm[a2] = pg[a2] = i2;
+            pm[d] = side ? n[d] - 1 - m : m;
+            pg[d] = side ? n[d] + m : -1 - m;
+            double mv[5], gv[5];
+            for (int v = 0; v < 5; ++v) mv[v] = q[gidx(gr, v, pm[0], pm[1], pm[2])];
+            wall_mirror(g, mv, gv);
+            for (int v = 0; v < 5; ++v) q[gidx(gr, v, pg[0], pg[1], pg[2])] = gv[v];
+          }
+  }
+  /* 2. periodic axes over the full extended range: copy from the periodic image */
   for (int v = 0; v < 5; ++v)
-    for (int k = -OR_NG; k < nz + OR_NG; ++k)
-      for (int j = -OR_NG; j < ny + OR_NG; ++j)
-        for (int i = -OR_NG; i < nx + OR_NG; ++i) {
-          int ii = wrap(i, nx), jj = wrap(j, ny), kk = wrap(k, nz);
-          if (ii == i && jj == j && kk == k) continue;
-          q[gidx(gr, v, i, j, k)] = q[gidx(gr, v, ii, jj, kk)];
+    for (int k = -OR_NG; k < n[2] + OR_NG; ++k)
+      for (int j = -OR_NG; j < n[1] + OR_NG; ++j)
+        for (int i = -OR_NG; i < n[0] + OR_NG; ++i) {
+          int c[3] = {i, j, k}, s[3] = {i, j, k}, moved = 0;
+          for (int d = 0; d < 3; ++d)
+            if (gr->bc[d] == 0) {
+              s[d] = wrap(c[d], n[d]);
+              moved |= s[d] != c[d];
+            }
+          if (moved) q[gidx(gr, v, c[0], c[1], c[2])] = q[gidx(gr, v, s[0], s[1], s[2])];
         }
 }
 
@@ -464,7 +574,6 @@ int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt, 
                 double* dL) {
   int nx = gr->n[0], ny = gr->n[1], nz = gr->n[2];
   long ncell = (long)nx * ny * nz;
-  double vol = gr->dx[0] * gr->dx[1] * gr->dx[2];
   for (long s = 0; s < 5 * ncell; ++s) {
     L[s] = 0.0;
     dL[s] = 0.0;
@@ -476,8 +585,6 @@ int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt, 
     nf[d] += 1; /* faces along d */
     long nface = (long)nf[0] * nf[1] * nf[2];
     double* Fd = (double*)malloc(sizeof(double) * 10 * nface);
-    double h[3] = {gr->dx[d], gr->dx[t1], gr->dx[t2]};
-    double area = gr->dx[t1] * gr->dx[t2];
 #pragma omp parallel for collapse(2) schedule(dynamic) reduction(| : fail)
     for (int fk = 0; fk < nf[2]; ++fk)
       for (int fj = 0; fj < nf[1]; ++fj)
@@ -498,8 +605,13 @@ int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt, 
                 cells[n][a][b][3] = q[gidx(gr, 1 + t2, p[0], p[1], p[2])];
                 cells[n][a][b][4] = q[gidx(gr, 4, p[0], p[1], p[2])];
               }
+          /* metrics (O-18): normal at the face, tangential at the Gauss abscissae */
+          double s3 = sqrt(3.0) / 6.0;
+          double Jn = or_axis_metric(gr, d, (double)f[d]);
+          double Jt1[2] = {or_axis_metric(gr, t1, f[t1] + 0.5 - s3), or_axis_metric(gr, t1, f[t1] + 0.5 + s3)};
+          double Jt2[2] = {or_axis_metric(gr, t2, f[t2] + 0.5 - s3), or_axis_metric(gr, t2, f[t2] + 0.5 + s3)};
           double Wl[4][5], Wr[4][5], dWl[4][3][5], dWr[4][3][5], dW0[4][3][5];
-          or_face_gauss_points((const double(*)[5][5][5])cells, h, Wl, Wr, dWl, dWr, dW0);
+          or_face_gauss_points((const double(*)[5][5][5])cells, Jn, Jt1, Jt2, Wl, Wr, dWl, dWr, dW0);
           double Fs[5] = {0, 0, 0, 0, 0}, dFs[5] = {0, 0, 0, 0, 0};
           for (int gp = 0; gp < 4; ++gp) { /* (m, n) order, O-21 */
             double F[5], dF[5];
@@ -514,7 +626,8 @@ int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt, 
               dFs[c] += 0.25 * dF[c];
             }
           }
-          /* rotate back to global components, times the face area */
+          /* rotate back to global components, times the physical face area */
+          double area = cell_width(gr, t1, f[t1]) * cell_width(gr, t2, f[t2]);
           int gc[5] = {0, 1 + d, 1 + t1, 1 + t2, 4};
           long fid = ((long)fk * nf[1] + fj) * nf[0] + fi;
           for (int c = 0; c < 5; ++c) {
@@ -528,6 +641,7 @@ int or_operator(const or_gas* g, const or_grid* gr, const double* q, double dt, 
         for (int i = 0; i < nx; ++i) {
           int lo[3] = {i, j, k}, hi[3] = {i, j, k};
           hi[d] += 1;
+          double vol = cell_width(gr, 0, i) * cell_width(gr, 1, j) * cell_width(gr, 2, k);
           long flo = ((long)lo[2] * nf[1] + lo[1]) * nf[0] + lo[0];
           long fhi = ((long)hi[2] * nf[1] + hi[1]) * nf[0] + hi[0];
           for (int c = 0; c < 5; ++c) {
@@ -565,8 +679,9 @@ double or_cfl_dt(const or_gas* g, const or_grid* gr, const double* q, double cfl
     double rho = q[s], U[3] = {q[ncell + s] / rho, q[2 * ncell + s] / rho, q[3 * ncell + s] / rho};
     double p = (g->gamma - 1.0) * (q[4 * ncell + s] - 0.5 * rho * (U[0] * U[0] + U[1] * U[1] + U[2] * U[2]));
     double c = sqrt(g->gamma * p / rho);
+    int ijk[3] = {(int)(s % gr->n[0]), (int)((s / gr->n[0]) % gr->n[1]), (int)(s / ((long)gr->n[0] * gr->n[1]))};
     for (int d = 0; d < 3; ++d) {
-      double v = gr->dx[d] / (fabs(U[d]) + c);
+      double v = cell_width(gr, d, ijk[d]) / (fabs(U[d]) + c);
       if (v < best) best = v;
     }
   }
@@ -611,12 +726,12 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
     if (dt_hist) dt_hist[step] = dt;
     /* stage 1 at Q^n */
     to_ghosted(gr, q, qg);
-    or_fill_ghosts_periodic(gr, qg);
+    or_fill_ghosts(g, gr, qg);
     if (or_operator(g, gr, qg, dt, L, dL)) { rc = -1; break; }
     or_s2o4_stage1(5 * ncell, q, L, dL, dt, qs);
     /* stage 2 at Q* (same dt and windows, O-11) */
     to_ghosted(gr, qs, qg);
-    or_fill_ghosts_periodic(gr, qg);
+    or_fill_ghosts(g, gr, qg);
     if (or_operator(g, gr, qg, dt, Ls, dLs)) { rc = -1; break; }
     or_s2o4_final(5 * ncell, q, L, dL, dLs, dt, qn);
     if (!state_valid(g, ncell, qn)) { rc = -1; break; }

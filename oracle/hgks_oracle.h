@@ -23,21 +23,34 @@ extern "C" {
 #define OR_NG 3      /* ghost layers (O-16) */
 #define OR_NM 9      /* velocity-moment tables hold orders 0..8 */
 
-/* gas + transport model (P:202-204 gamma/K; P:270-273 tau=mu/p; P:971-973 power law) */
+/* gas + transport model (P:202-204 gamma/K; P:270-273 tau=mu/p; P:971-973 power law, Pr) */
 typedef struct {
   double gamma;   /* specific heat ratio                                         */
   double K;       /* internal DOF, or_K(gamma) (O-20)                      */
-  double prandtl; /* Pr; 1 = no heat-flux fix (TGV)                        */
+  double prandtl; /* Pr; 1 = no heat-flux fix (TGV); != 1: O-12 fix        */
   int    mu_law;  /* 0: mu = mu_ref ; 1: mu = mu_ref*(T/T_ref)^omega, T = p/rho     */
   double mu_ref, T_ref, omega;
+  double T_wall;  /* isothermal wall temperature (p/rho units), O-17              */
 } or_gas;
 
-/* uniform-grid geometry of a block that carries OR_NG ghost layers on every side */
+/* Geometry of a block that carries OR_NG ghost layers on every side.  Axis d is uniform
+ * (stretch 0: width dx[d]) or tanh-stretched (stretch 1):
+ *   x(s) = (lo+hi)/2 + (hi-lo)/2 * tanh(b (2 s - 1)) / tanh(b),  s = j / n[d] at face j,
+ * i.e. uniform in the computational coordinate (the paper's eta / (3 pi) for the channel). */
 typedef struct {
-  int    n[3];     /* interior cells nx, ny, nz                 */
-  double dx[3];    /* cell widths                               */
-  int    bc[3];    /* 0 periodic (only periodic is implemented) */
+  int    n[3];          /* interior cells nx, ny, nz                                    */
+  double dx[3];         /* cell widths of uniform axes                                  */
+  int    bc[3];         /* 0 periodic, 1 isothermal no-slip walls at both ends (O-17)   */
+  int    stretch[3];    /* 0 uniform, 1 tanh                                            */
+  double lo[3], hi[3];  /* box of stretched axes                                        */
+  double stretch_b[3];  /* b_g of tanh axes (b_g = 2)                            */
 } or_grid;
+
+/* Face coordinate x_j (j = 0..n[d]), and the metric J = d(cell index)/dx at fractional cell-index
+ * position zeta (zeta = j at face j, j + 1/2 at the centre of cell j) of axis d.  J = 1/dx on
+ * uniform axes; the analytic derivative of the tanh map otherwise (O-18).  Pin: Tables 6-7. */
+double or_axis_face(const or_grid* gr, int d, int j);
+double or_axis_metric(const or_grid* gr, int d, double zeta);
 
 double or_K(double gamma);
 
@@ -81,17 +94,20 @@ double or_weno5z_right(const double q[5]);
 double or_weno5z_left(const double q[5]);
 
 /* Gauss-point inputs of one face from a 6 (normal) x 5 (t1) x 5 (t2) block of cell averages
- * cells[n][a][b] (n = i-2..i+3 normal, a = t1 offset -2..2, b = t2 offset -2..2), with cell
- * widths h = (h_n, h_t1, h_t2).  For Gauss point gp = 2*m + n (m index in t1, n in t2, point
- * -sqrt(3)/6 first), component c:
+ * cells[n][a][b] (n = i-2..i+3 normal, a = t1 offset -2..2, b = t2 offset -2..2).  Derivatives are
+ * taken in cell-index units (reconstruction in the computational coordinate, O-18) and converted
+ * with the metrics: Jn at the face (normal), Jt1[m], Jt2[n] at the Gauss abscissae.  For Gauss point
+ * gp = 2*m + n (m index in t1, n in t2, point -sqrt(3)/6 first), component c:
  *   Wl[gp][c], Wr[gp][c], dWl[gp][i][c], dWr[gp][i][c], dW0[gp][i][c]   (i: normal, t1, t2)
- * Steps A2-A3 with readings O-3, O-4, O-6.  Pins: trilinear exactness, constants. */
-void or_face_gauss_points(const double cells[6][5][5][5], const double h[3],
-                          double Wl[4][5], double Wr[4][5], double dWl[4][3][5],
+ * Steps A2-A3 with readings O-3, O-4, O-6.  Pins: polynomial exactness, constants. */
+void or_face_gauss_points(const double cells[6][5][5][5], double Jn, const double Jt1[2],
+                          const double Jt2[2], double Wl[4][5], double Wr[4][5], double dWl[4][3][5],
                           double dWr[4][3][5], double dW0[4][3][5]);
 
-/* Whole-grid periodic ghost fill of q laid out [5][nz+6][ny+6][nx+6] (O-16). */
-void or_fill_ghosts_periodic(const or_grid* gr, double* q);
+/* Whole-grid ghost fill of q laid out [5][nz+6][ny+6][nx+6] (O-16, O-17): wall axes first over
+ * the interior of the other axes (mirror: U_g = -U_m, T_g = 2 T_wall - T_m, p_g = p_m), then the
+ * periodic axes over the full extended range (corners). */
+void or_fill_ghosts(const or_gas* g, const or_grid* gr, double* q);
 
 /* Operator L(Q) and d_t L(Q) (Eqs. (3)-(4)) on the interior of a ghosted
  * block q [5][nz+6][ny+6][nx+6] whose ghosts are already filled.  L, dL are [5][nz][ny][nx].
@@ -109,10 +125,11 @@ void or_s2o4_final(long n, const double* q, const double* L, const double* dL,
                    const double* dLs, double dt, double* qn);
 
 /* CFL time step (O-13): dt = cfl * min over cells, d of dx_d/(|U_d| + c), c = sqrt(gamma p/rho),
- * on an unghosted [5][nz][ny][nx] state.  Pin: Table 3. */
+ * with the cell's own width dx_d on stretched axes, on an unghosted [5][nz][ny][nx] state.
+ * Pin: Table 3. */
 double or_cfl_dt(const or_gas* g, const or_grid* gr, const double* q, double cfl);
 
-/* Full periodic S2O4 steps on an unghosted [5][nz][ny][nx] state, in place.
+/* Full S2O4 steps on an unghosted [5][nz][ny][nx] state, in place (ghosts by or_fill_ghosts).
  * dt_fixed > 0 uses it; else CFL each step.  dt_hist (nsteps, may be NULL) receives the dt
  * used.  Returns 0, or -1 on an invalid state (q then holds the last good state). */
 int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed,

@@ -36,11 +36,13 @@ def build(force: bool = False) -> str:
 class Gas(C.Structure):
     _fields_ = [("gamma", C.c_double), ("K", C.c_double), ("prandtl", C.c_double),
                 ("mu_law", C.c_int), ("mu_ref", C.c_double), ("T_ref", C.c_double),
-                ("omega", C.c_double)]
+                ("omega", C.c_double), ("T_wall", C.c_double)]
 
 
 class Grid(C.Structure):
-    _fields_ = [("n", C.c_int * 3), ("dx", C.c_double * 3), ("bc", C.c_int * 3)]
+    _fields_ = [("n", C.c_int * 3), ("dx", C.c_double * 3), ("bc", C.c_int * 3),
+                ("stretch", C.c_int * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+                ("stretch_b", C.c_double * 3)]
 
 
 _lib = None
@@ -63,8 +65,12 @@ def lib():
         L.or_weno5z_right.argtypes = [_dp]
         L.or_weno5z_left.restype = C.c_double
         L.or_weno5z_left.argtypes = [_dp]
-        L.or_face_gauss_points.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, _dp]
-        L.or_fill_ghosts_periodic.argtypes = [C.POINTER(Grid), _dp]
+        L.or_face_gauss_points.argtypes = [_dp, C.c_double, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.or_fill_ghosts.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp]
+        L.or_axis_face.restype = C.c_double
+        L.or_axis_face.argtypes = [C.POINTER(Grid), C.c_int, C.c_int]
+        L.or_axis_metric.restype = C.c_double
+        L.or_axis_metric.argtypes = [C.POINTER(Grid), C.c_int, C.c_double]
         L.or_operator.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double, _dp, _dp]
         L.or_s2o4_stage1.argtypes = [C.c_long, _dp, _dp, _dp, C.c_double, _dp]
         L.or_s2o4_final.argtypes = [C.c_long, _dp, _dp, _dp, _dp, C.c_double, _dp]
@@ -93,17 +99,31 @@ def K_of(gamma: float) -> float:
     return lib().or_K(gamma)
 
 
-def make_gas(gamma=1.4, mu=0.0, prandtl=1.0, mu_law=0, T_ref=1.0, omega=0.0) -> Gas:
-    return Gas(gamma, K_of(gamma), prandtl, mu_law, mu, T_ref, omega)
+def make_gas(gamma=1.4, mu=0.0, prandtl=1.0, mu_law=0, T_ref=1.0, omega=0.0, T_wall=1.0) -> Gas:
+    return Gas(gamma, K_of(gamma), prandtl, mu_law, mu, T_ref, omega, T_wall)
 
 
-def make_grid(n, dx) -> Grid:
+def make_grid(n, dx, bc=(0, 0, 0), stretch=(0, 0, 0), lo=(0.0, 0.0, 0.0), hi=None, stretch_b=(0.0, 0.0, 0.0)) -> Grid:
+    """n cells; dx widths of uniform axes; bc 0 periodic / 1 isothermal wall; stretch 1 = tanh
+    on [lo, hi] with b = stretch_b (P:945-956)."""
     g = Grid()
     for d in range(3):
         g.n[d] = int(n[d])
         g.dx[d] = float(dx[d])
-        g.bc[d] = 0
+        g.bc[d] = int(bc[d])
+        g.stretch[d] = int(stretch[d])
+        g.lo[d] = float(lo[d])
+        g.hi[d] = float(hi[d]) if hi is not None else float(lo[d]) + n[d] * float(dx[d])
+        g.stretch_b[d] = float(stretch_b[d])
     return g
+
+
+def axis_faces(grid: Grid, d: int) -> np.ndarray:
+    return np.array([lib().or_axis_face(C.byref(grid), d, j) for j in range(grid.n[d] + 1)])
+
+
+def axis_metric(grid: Grid, d: int, zeta: float) -> float:
+    return lib().or_axis_metric(C.byref(grid), d, zeta)
 
 
 def moments_u(U, lam, which):
@@ -155,35 +175,46 @@ def weno5z(q, side="right"):
     return f(_p(q))
 
 
-def face_gauss_points(cells, h):
-    """cells: [6 normal][5 t1][5 t2][5 comp] -> dict of GP inputs."""
-    cells, h = _arr(cells, (6, 5, 5, 5)), _arr(h, (3,))
+def face_gauss_points(cells, h=None, J=None):
+    """cells: [6 normal][5 t1][5 t2][5 comp] -> dict of GP inputs.  Uniform widths h = (hn, h1, h2)
+    or metrics J = (Jn, [Jt1_m0, Jt1_m1], [Jt2_n0, Jt2_n1])."""
+    cells = _arr(cells, (6, 5, 5, 5))
+    if J is None:
+        J = (1.0 / h[0], [1.0 / h[1]] * 2, [1.0 / h[2]] * 2)
+    Jt1, Jt2 = _arr(J[1], (2,)), _arr(J[2], (2,))
     Wl, Wr = np.zeros((4, 5)), np.zeros((4, 5))
     dWl, dWr, dW0 = np.zeros((4, 3, 5)), np.zeros((4, 3, 5)), np.zeros((4, 3, 5))
-    lib().or_face_gauss_points(_p(cells), _p(h), _p(Wl), _p(Wr), _p(dWl), _p(dWr), _p(dW0))
+    lib().or_face_gauss_points(_p(cells), float(J[0]), _p(Jt1), _p(Jt2), _p(Wl), _p(Wr), _p(dWl),
+                               _p(dWr), _p(dW0))
     return dict(Wl=Wl, Wr=Wr, dWl=dWl, dWr=dWr, dW0=dW0)
 
 
-def ghosted(q: np.ndarray, ng: int = 3) -> np.ndarray:
-    """[5][nz][ny][nx] -> [5][nz+6][ny+6][nx+6] with periodic ghosts filled by the oracle."""
+def _grid_of(q, dx, grid):
+    _, nz, ny, nx = q.shape
+    return grid if grid is not None else make_grid((nx, ny, nz), dx)
+
+
+def ghosted(q: np.ndarray, ng: int = 3, gas: Gas | None = None, grid: Grid | None = None) -> np.ndarray:
+    """[5][nz][ny][nx] -> [5][nz+6][ny+6][nx+6] with ghosts filled by the oracle (periodic unless
+    grid says walls)."""
     q = _arr(q)
     _, nz, ny, nx = q.shape
     qg = np.zeros((5, nz + 2 * ng, ny + 2 * ng, nx + 2 * ng))
     qg[:, ng:-ng, ng:-ng, ng:-ng] = q
-    lib().or_fill_ghosts_periodic(C.byref(make_grid((nx, ny, nz), (1, 1, 1))), _p(qg))
+    gr = grid if grid is not None else make_grid((nx, ny, nz), (1, 1, 1))
+    lib().or_fill_ghosts(C.byref(gas if gas is not None else make_gas()), C.byref(gr), _p(qg))
     return qg
 
 
-def operator(gas: Gas, q: np.ndarray, dx, dt: float, qg: np.ndarray | None = None):
-    """L(Q), d_t L(Q) for a periodic state (or a pre-ghosted block qg)."""
+def operator(gas: Gas, q: np.ndarray, dx, dt: float, qg: np.ndarray | None = None, grid: Grid | None = None):
+    """L(Q), d_t L(Q) for a state (periodic unless grid has walls) or a pre-ghosted block qg."""
     q = _arr(q)
-    _, nz, ny, nx = q.shape
+    gr = _grid_of(q, dx, grid)
     if qg is None:
-        qg = ghosted(q)
+        qg = ghosted(q, gas=gas, grid=gr)
     qg = _arr(qg)
     L, dL = np.zeros_like(q), np.zeros_like(q)
-    rc = lib().or_operator(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(qg), dt, _p(L),
-                           _p(dL))
+    rc = lib().or_operator(C.byref(gas), C.byref(gr), _p(qg), dt, _p(L), _p(dL))
     if rc:
         raise ValueError("invalid state inside operator")
     return L, dL
@@ -203,18 +234,18 @@ def s2o4_final(q, L, dL, dLs, dt):
     return qn
 
 
-def cfl_dt(gas: Gas, q: np.ndarray, dx, cfl: float = 0.4) -> float:
+def cfl_dt(gas: Gas, q: np.ndarray, dx, cfl: float = 0.4, grid: Grid | None = None) -> float:
     q = _arr(q)
-    _, nz, ny, nx = q.shape
-    return lib().or_cfl_dt(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(q), cfl)
+    return lib().or_cfl_dt(C.byref(gas), C.byref(_grid_of(q, dx, grid)), _p(q), cfl)
 
 
-def run(gas: Gas, q: np.ndarray, dx, nsteps: int, dt_fixed: float = 0.0, cfl: float = 0.4):
-    """Advance a periodic state nsteps full S2O4 steps; returns (q_new, dt_history)."""
+def run(gas: Gas, q: np.ndarray, dx, nsteps: int, dt_fixed: float = 0.0, cfl: float = 0.4,
+        grid: Grid | None = None):
+    """Advance a state nsteps full S2O4 steps (periodic unless grid has walls); returns
+    (q_new, dt_history)."""
     q = _arr(q).copy()
-    _, nz, ny, nx = q.shape
     hist = np.zeros(max(nsteps, 1))
-    rc = lib().or_run(C.byref(gas), C.byref(make_grid((nx, ny, nz), dx)), _p(q), nsteps, dt_fixed,
+    rc = lib().or_run(C.byref(gas), C.byref(_grid_of(q, dx, grid)), _p(q), nsteps, dt_fixed,
                       cfl, _p(hist))
     if rc:
         raise ValueError("oracle run hit an invalid state")

@@ -131,3 +131,61 @@ def perturbed(n, seed: int = 0, amp: float = 0.05, modes: int = 3, base=(1.0, 0.
             prim.append(base[v] + amp * f)
     dx = (length / nx, length / ny, length / nz)
     return np.ascontiguousarray(prim_to_cons(*prim, gamma=gamma)), dx
+
+
+# ------------------------------------------------------------------------------------------------
+# Channel flow (BASELINE config 4): [0, 2 pi H] x [-H, H] x [0, pi H], tanh-stretched y
+# (b_g = 2), isothermal no-slip walls at y = -H, H, periodic x and z.  Units rho_b = U_b = H = 1.
+# Bulk Re = 3000 (Re_tau ~ 180 by the H-series meshes) -> mu_w = 1/3000; bulk Mach 0.5
+# (BASELINE config 4) -> T_w = (U_b/Ma)^2 / gamma in T = p/rho units; mu = mu_w (T/T_w)^0.7,
+# Pr = 0.7.  Initial state: rho = 1, T = T_w, U = 1.5 (1 - y^2) plus 10% white noise
+# of the local U, V and W white noise of 0.1 U_b, noise from a counter-based hash of
+# (seed, global cell index) so the field does not depend on the decomposition.
+# ------------------------------------------------------------------------------------------------
+CHANNEL_SEED = 20220705
+
+
+def channel_params(ma: float = 0.5, re_b: float = 3000.0, gamma: float = GAMMA):
+    T_w = (1.0 / ma) ** 2 / gamma
+    return dict(gamma=gamma, T_w=T_w, mu_w=1.0 / re_b, omega=0.7, prandtl=0.7, b_g=2.0,
+                lo=(0.0, -1.0, 0.0), hi=(2 * math.pi, 1.0, math.pi), ma=ma, re_b=re_b)
+
+
+def tanh_faces(n: int, lo: float, hi: float, b: float) -> np.ndarray:
+    """Face coordinates of the tanh map: x_j = c + h tanh(b(2 j/n - 1))/tanh(b)."""
+    s = np.arange(n + 1) / n
+    return 0.5 * (lo + hi) + 0.5 * (hi - lo) * np.tanh(b * (2 * s - 1)) / np.tanh(b)
+
+
+def _unit_noise(seed: int, idx: np.ndarray, stream: int) -> np.ndarray:
+    """uniform [-1, 1) from splitmix64(seed, stream, global index): counter-based."""
+    with np.errstate(over="ignore"):
+        z = (idx.astype(np.uint64) + np.uint64(stream) * np.uint64(0x9E3779B97F4A7C15)
+             + np.uint64(seed) * np.uint64(0xD1B54A32D192ED03))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) / float(1 << 53) * 2.0 - 1.0
+
+
+def channel(n, z_begin: int = 0, nz_local: int | None = None, seed: int = CHANNEL_SEED, noise: float = 0.1,
+            ma: float = 0.5, re_b: float = 3000.0, gamma: float = GAMMA):
+    """Perturbed Poiseuille initial field of the channel (config 4).  Returns (q, params) with
+    q [5][nz_local][ny][nx]; y cell centres are the midpoints of the tanh faces."""
+    nx, ny, nz = n
+    if nz_local is None:
+        nz_local = nz - z_begin
+    prm = channel_params(ma=ma, re_b=re_b, gamma=gamma)
+    yf = tanh_faces(ny, -1.0, 1.0, prm["b_g"])
+    yc = 0.5 * (yf[1:] + yf[:-1])
+    k = np.arange(z_begin, z_begin + nz_local)
+    K_, J_, I_ = np.meshgrid(k, np.arange(ny), np.arange(nx), indexing="ij")
+    gid = (K_.astype(np.int64) * ny + J_) * nx + I_
+    Y = yc[J_]
+    Ub = 1.5 * (1.0 - Y * Y)
+    U = Ub * (1.0 + noise * _unit_noise(seed, gid, 1))
+    V = noise * _unit_noise(seed, gid, 2)
+    W = noise * _unit_noise(seed, gid, 3)
+    rho = np.ones_like(U)
+    p = rho * prm["T_w"]
+    return np.ascontiguousarray(prim_to_cons(rho, U, V, W, p, gamma)), prm
