@@ -47,16 +47,26 @@ typedef enum {
 
 typedef enum { HGKS_FP64 = 0, HGKS_FP32 = 1 } hgks_precision;      /* P:1091-1093 FP32/FP64 builds */
 typedef enum { HGKS_PERIODIC = 0, HGKS_WALL_ISOTHERMAL = 1 } hgks_bc;
+typedef enum { HGKS_UNIFORM = 0, HGKS_TANH = 1 } hgks_stretch;       /* P:945-956 channel mesh        */
 typedef enum { HGKS_MU_CONST = 0, HGKS_MU_POWER = 1 } hgks_mu_law;
 
 typedef struct {
   int32_t n[3];          /* GLOBAL interior cells (nx, ny, nz); each >= 5; nz/nranks >= 3           */
-  double lo[3], hi[3];   /* box: uniform spacing dx_d = (hi_d - lo_d)/n_d                           */
-  hgks_bc bc[3];         /* per axis (both ends); only HGKS_PERIODIC is accepted in this build      */
+  double lo[3], hi[3];   /* box [lo_d, hi_d]                                                        */
+  hgks_bc bc[3];         /* per axis (both ends).  Walls: x or y only (z is the slab axis).  A wall
+                            axis gets isothermal no-slip mirror ghosts (reading O-17):
+                            U_g = -U_m, T_g = 2 T_wall - T_m, p_g = p_m                              */
+  hgks_stretch stretch[3]; /* HGKS_UNIFORM: dx = (hi-lo)/n.  HGKS_TANH (reading O-18):
+                            faces x_j = (lo+hi)/2 + (hi-lo)/2 tanh(b(2j/n - 1))/tanh(b); the
+                            reconstruction runs in the uniform cell-index coordinate and derivatives
+                            use the analytic metric of the map; x or y only                        */
+  double stretch_b[3];   /* b of HGKS_TANH axes (the paper's b_g = 2)                              */
   double gamma;          /* 1 < gamma <= 5/3 ; K = (5 - 3 gamma)/(gamma - 1)              */
-  double prandtl;        /* Pr; only Pr == 1 is accepted in this build                     */
+  double prandtl;        /* Pr > 0; Pr != 1 adds (1/Pr - 1) q to the energy flux,
+                            q the heat flux of the interface distribution relative to U0 (O-12)   */
   hgks_mu_law mu_law;    /* mu = mu_ref (const) or mu_ref (T/T_ref)^omega with T = p/rho          */
   double mu_ref, T_ref, omega;
+  double T_wall;         /* wall temperature (T = p/rho units) of HGKS_WALL_ISOTHERMAL axes        */
   double cfl;            /* > 0: adaptive dt = cfl / max_cells max_d (|U_d| + c)/dx_d (O-13)       */
   double dt_fixed;       /* > 0: fixed dt, overrides cfl (parity / timing runs)                    */
   hgks_precision precision;

@@ -17,10 +17,11 @@ extern "C" {
 /* Batched Gauss-point flux (steps A4-A6; Eq. (6) P:252-258 + Eq. (8)), local frame.
  *   in  : n records of 55 fp64 = Wl[5], Wr[5], dWl[3][5], dWr[3][5], dW0[3][5] (i: normal,t1,t2)
  *   out : n records of 11 fp64 = F[5], dF[5], tau
- *   gamma, mu_law/mu_ref/T_ref/omega as in hgks_params; dt the step (windows [0,dt/2], [0,dt]).
- * Returns HGKS_OK or HGKS_ECUDA / HGKS_EINVAL. */
+ *   gamma, mu_law/mu_ref/T_ref/omega, prandtl as in hgks_params; dt the step (windows [0,dt/2],
+ *   [0,dt]).  Returns HGKS_OK or HGKS_ECUDA / HGKS_EINVAL. */
 int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, double T_ref,
-                      double omega, double dt, const double* in, int64_t n, double* out);
+                      double omega, double prandtl, double dt, const double* in, int64_t n,
+                      double* out);
 
 /* Operator evaluation on the context's current state (after hgks_set_state): one ghost fill and
  * the three flux sweeps at time step dt, then L(Q) and d_t L(Q) (Eqs. (3)-(4), P:211-218,

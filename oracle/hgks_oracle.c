@@ -537,8 +537,11 @@ void or_fill_ghosts(const or_gas* g, const or_grid* gr, double* q) {
   for (int d = 0; d < 3; ++d) {
     if (gr->bc[d] != 1) continue;
     int a1 = (d + 1) % 3, a2 = (d + 2) % 3;
-    for (int i2 = 0; i2 < n[a2]; ++i2)
-      for (int i1 = 0; i1 < n[a1]; ++i1)
+    /* interior of the other axes; their whole extended range when their ghosts are supplied (bc 2) */
+    int lo1 = gr->bc[a1] == 2 ? -OR_NG : 0, hi1 = n[a1] + (gr->bc[a1] == 2 ? OR_NG : 0);
+    int lo2 = gr->bc[a2] == 2 ? -OR_NG : 0, hi2 = n[a2] + (gr->bc[a2] == 2 ? OR_NG : 0);
+    for (int i2 = lo2; i2 < hi2; ++i2)
+      for (int i1 = lo1; i1 < hi1; ++i1)
         for (int m = 0; m < OR_NG; ++m)
           for (int side = 0; side < 2; ++side) {
             int pm[3], pg[3];
@@ -552,7 +555,8 @@ void or_fill_ghosts(const or_gas* g, const or_grid* gr, double* q) {
             for (int v = 0; v < 5; ++v) q[gidx(gr, v, pg[0], pg[1], pg[2])] = gv[v];
           }
   }
-  /* 2. periodic axes over the full extended range: copy from the periodic image */
+  /* 2. periodic axes over the full extended range: copy from the periodic image
+   *    (bc 2 = ghosts supplied by the caller, e.g. a sub-block cut from a larger field: untouched) */
   for (int v = 0; v < 5; ++v)
     for (int k = -OR_NG; k < n[2] + OR_NG; ++k)
       for (int j = -OR_NG; j < n[1] + OR_NG; ++j)

@@ -40,7 +40,8 @@ typedef struct {
 typedef struct {
   int    n[3];          /* interior cells nx, ny, nz                                    */
   double dx[3];         /* cell widths of uniform axes                                  */
-  int    bc[3];         /* 0 periodic, 1 isothermal no-slip walls at both ends (O-17)   */
+  int    bc[3];         /* 0 periodic, 1 isothermal no-slip walls at both ends (O-17),
+                           2 ghosts supplied by the caller (sub-blocks in tests)          */
   int    stretch[3];    /* 0 uniform, 1 tanh                                            */
   double lo[3], hi[3];  /* box of stretched axes                                        */
   double stretch_b[3];  /* b_g of tanh axes (b_g = 2)                            */

@@ -99,6 +99,7 @@ struct GasK {
   T gamma;
   T mu_ref, T_ref, omega;
   int mu_law;  // 0 const, 1 power law
+  T prf;       // 1/Pr - 1 (heat-flux fix, O-12; used by GpFlux<.., PRF = true>)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -258,19 +259,20 @@ HD void temporal_slope(T K, T th, T it, const T (&R)[5], T (&A)[5]) {
 //   add_side<+1>(load_l), add_side<-1>(load_r)   g_l H(u) and g_r (1 - H(u)) terms (Gamma_4..6)
 //   add_equilibrium(load_0)        g0 terms of Eq. (6) (Gamma_1..3)
 // Results: F (if NEED_F), dF, tau.  Invalid input propagates as NaN.
-template <typename T, bool NEED_F>
+template <typename T, bool NEED_F, bool PRF = false>
 struct GpFlux {
   T K;
   T rl, irl, Ul, Vl, Wl, thl, hl0, hl1;
   T rr, irr, Ur, Vr, Wr, thr, hr0, hr1;
   T r0, ir0, U0, V0, W0, th0;
-  T h, idt, dt;
+  T h, idt, dt, prf;
   T F[5], dF[5], tau;
 
   HD void begin(const GasK<T>& g, const T (&WL)[5], const T (&WR)[5], T dt_, T idt_) {
     K = g.K;
     dt = dt_;
     idt = idt_;
+    prf = g.prf;
     const T isqpi = T(0.56418958354775628694807945156077);  // 1/sqrt(pi)
     const T k3 = T(4) * rcp(K + T(3));
     rl = WL[0];
@@ -407,6 +409,13 @@ struct GpFlux {
     Y[2] = -U0 * R[2];
     Y[3] = -U0 * R[3];
     Y[4] = -U0 * R[4] + hK5t * th * A[1];
+    if (PRF) {  // heat flux relative to U0 (O-12): energy component of <c_x ... psi_c>
+      const T qx = X[4], qy = Y[4] + U0 * R[4];  // X[4] before the U0 R shift = X_c[4] - U0 R[4]
+      T ga, gb, gc, gpa, gpb, gpc;
+      gammas(true, ga, gb, gc, gpa, gpb, gpc);
+      dF[4] += r0 * prf * (gpb * qx + gpc * qy);
+      if (NEED_F) F[4] += r0 * prf * (gb * qx + gc * qy);
+    }
 #pragma unroll
     for (int k = 0; k < 5; ++k) X[k] += U0 * R[k];
     T Z[5] = {U0, th, T(0), T(0), U0 * hK3};
@@ -446,6 +455,7 @@ struct GpFlux {
     T R[5] = {T(0), T(0), T(0), T(0), T(0)};
     T X[5] = {T(0), T(0), T(0), T(0), T(0)};
     const T g3 = T(0.5) * th * (t[3] + k4 * t[1]);
+    T ad[3][5];  // slopes kept for the heat-flux density moments (PRF only; dead otherwise)
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       T dW[5], a[5];
@@ -454,6 +464,10 @@ struct GpFlux {
       if (i == 1) slope_dir<1>(K, irho, U, V, W, th, it, dW, a, R);
       if (i == 2) slope_dir<2>(K, irho, U, V, W, th, it, dW, a, R);
       to_t(a);
+      if (PRF) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) ad[i][k] = a[k];
+      }
       if (i == 0) {
         H(a, 2, T(1), X);
       } else if (i == 1) {  // V H_1(a) + G_v(a)
@@ -476,15 +490,47 @@ struct GpFlux {
     T Y[5] = {T(0), T(0), T(0), T(0), T(0)};
     H(A, 1, T(1), Y);
     T Z[5] = {t[1], t[2], T(0), T(0), T(0.5) * (t[3] + k2 * t[1])};
+    if (PRF) {
+      // heat flux relative to U0 (O-12) from the flux vectors (Z, X, Y) and the density vectors
+      // (Zd, Xd, Yd) = <psi>, sum_i <u_i a_i.psi psi>, <A.psi psi> of this side, all in its
+      // tangential frame; d = U0 - (0, V, W) is the equilibrium velocity seen from that frame
+      T Xd[5] = {T(0), T(0), T(0), T(0), T(0)}, Yd[5] = {T(0), T(0), T(0), T(0), T(0)};
+      H(A, 0, T(1), Yd);
+      H(ad[0], 1, T(1), Xd);
+      H(ad[1], 0, V, Xd);
+      H(ad[2], 0, W, Xd);
+      const T g0 = T(0.5) * th * (t[2] + k4 * t[0]);
+      Xd[0] += th * t[0] * (ad[1][2] + ad[2][3]);
+      Xd[1] += th * t[1] * (ad[1][2] + ad[2][3]);
+      Xd[2] += th * f(ad[1], 0);
+      Xd[3] += th * f(ad[2], 0);
+      Xd[4] += g0 * (ad[1][2] + ad[2][3]);
+      const T Zd[5] = {t[0], t[1], T(0), T(0), T(0.5) * (t[2] + k2 * t[0])};
+      const T dx = U0, dy = V0 - V, dz = W0 - W, d2 = T(0.5) * (dx * dx + dy * dy + dz * dz);
+      auto heat = [&](T a, T b, T c) {
+        T Fv[5], Wv[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          Fv[k] = a * Z[k] + b * X[k] + c * Y[k];
+          Wv[k] = a * Zd[k] + b * Xd[k] + c * Yd[k];
+        }
+        return Fv[4] - (dx * Fv[1] + dy * Fv[2] + dz * Fv[3]) + d2 * Fv[0] -
+               dx * (Wv[4] - (dx * Wv[1] + dy * Wv[2] + dz * Wv[3]) + d2 * Wv[0]);
+      };
+      T ga, gb, gc, gpa, gpb, gpc;
+      gammas(false, ga, gb, gc, gpa, gpb, gpc);
+      dF[4] += rho * prf * heat(gpa, gpb, gpc);
+      if (NEED_F) F[4] += rho * prf * heat(ga, gb, gc);
+    }
     accumulate(false, rho, T(0), V, W, Z, X, Y);
   }
 };
 
 // One-call form (tests and the batched test entry point).
-template <typename T, bool NEED_F>
+template <typename T, bool NEED_F, bool PRF = false>
 HD void gp_flux(const GasK<T>& g, const T (&Wl)[5], const T (&Wr)[5], const T (&dWl)[3][5], const T (&dWr)[3][5],
                 const T (&dW0)[3][5], T dt, T (&F)[5], T (&dF)[5], T& tau) {
-  GpFlux<T, NEED_F> gf;
+  GpFlux<T, NEED_F, PRF> gf;
   gf.begin(g, Wl, Wr, dt, T(1) / dt);
   gf.template add_side<+1>([&](int i, T (&d)[5]) { for (int k = 0; k < 5; ++k) d[k] = dWl[i][k]; });
   gf.template add_side<-1>([&](int i, T (&d)[5]) { for (int k = 0; k < 5; ++k) d[k] = dWr[i][k]; });

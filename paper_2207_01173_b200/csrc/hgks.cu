@@ -48,6 +48,8 @@ struct hgks_ctx {
   void* Q[2] = {nullptr, nullptr};
   void* Qs = nullptr;
   void* F[3] = {nullptr, nullptr, nullptr};
+  void* metric = nullptr;   // per axis: jf[n+1], jg[2n], iw[n] (T), see Geo
+  size_t metric_off[3][3] = {};
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
   cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
@@ -128,7 +130,42 @@ static Geo<T> make_geo(const hgks_ctx* c) {
   g.z0 = c->z0;
   g.nx_g = c->n[0];
   g.ny_g = c->n[1];
+  for (int d = 0; d < 3; ++d) {
+    const T* base = (const T*)c->metric;
+    g.jf[d] = base + c->metric_off[d][0];
+    g.jg[d] = base + c->metric_off[d][1];
+    g.iw[d] = base + c->metric_off[d][2];
+    g.wall[d] = c->p.bc[d] == HGKS_WALL_ISOTHERMAL;
+  }
+  g.T_wall = T(c->p.T_wall);
   return g;
+}
+
+// Metric tables of one axis (reading O-18), computed here in fp64: the reconstruction works in the
+// uniform cell-index coordinate zeta (face j at zeta = j); J = d zeta / dx.  For HGKS_TANH,
+// x(zeta) = (lo+hi)/2 + (hi-lo)/2 tanh(b (2 zeta/N - 1)) / tanh(b).
+static void axis_tables(const hgks_params& p, int d, int N, int j0, int n, double* jf, double* jg, double* iw) {
+  const double lo = p.lo[d], hi = p.hi[d];
+  if (p.stretch[d] != HGKS_TANH) {
+    const double ih = N / (hi - lo);
+    for (int j = 0; j <= n; ++j) jf[j] = ih;
+    for (int j = 0; j < 2 * n; ++j) jg[j] = ih;
+    for (int j = 0; j < n; ++j) iw[j] = ih;
+    return;
+  }
+  const double b = p.stretch_b[d], tb = tanh(b), hh = 0.5 * (hi - lo), cc = 0.5 * (lo + hi);
+  auto x = [&](double z) { return cc + hh * tanh(b * (2.0 * z / N - 1.0)) / tb; };
+  auto J = [&](double z) {
+    const double ch = cosh(b * (2.0 * z / N - 1.0));
+    return 1.0 / (hh / tb * b * (2.0 / N) / (ch * ch));
+  };
+  const double s3 = sqrt(3.0) / 6.0;
+  for (int j = 0; j <= n; ++j) jf[j] = J(j0 + j);
+  for (int j = 0; j < n; ++j) {
+    jg[j] = J(j0 + j + 0.5 - s3);
+    jg[n + j] = J(j0 + j + 0.5 + s3);
+    iw[j] = 1.0 / (x(j0 + j + 1) - x(j0 + j));
+  }
 }
 
 template <typename T>
@@ -140,6 +177,7 @@ static GasK<T> make_gas(const hgks_params& p) {
   g.T_ref = T(p.T_ref > 0 ? p.T_ref : 1.0);
   g.omega = T(p.omega);
   g.mu_law = (int)p.mu_law;
+  g.prf = T(1.0 / p.prandtl - 1.0);
   return g;
 }
 
@@ -151,6 +189,11 @@ static int fill_ghosts(hgks_ctx* c, T* q) {
   Geo<T> g = make_geo<T>(c);
   long long total = (long long)g.n[2] * g.plane;
   prof_begin(c, HGKS_K_GHOST);
+  if (g.wall[0] || g.wall[1]) {
+    ghost_wall_kernel<T><<<blocks_for((long long)g.n[2] * 6 * std::max(g.n[0], g.n[1]), 256), 256, 0, c->s>>>(
+        q, g, c->p.gamma, c->ctl);
+    c->total_launches += 1;
+  }
   ghost_xy_kernel<T><<<blocks_for(total, 256), 256, 0, c->s>>>(q, g, c->ctl);
   prof_end(c, HGKS_K_GHOST);
   c->total_launches += 1;
@@ -182,9 +225,13 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   static bool attr_done[2][2] = {{false, false}, {false, false}};
   const int pi = sizeof(T) == 8 ? 0 : 1;
   if (!attr_done[pi][STAGE - 1]) {
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int sm = (int)smem;
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr_done[pi][STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
@@ -212,9 +259,13 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, n3[d] + 1);
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
-    if (d == 0) flux_kernel<T, 0, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
-    if (d == 1) flux_kernel<T, 1, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
-    if (d == 2) flux_kernel<T, 2, STAGE><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
+    const bool prf = c->p.prandtl != 1.0;
+    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
+    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
+    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
+    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
+    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
+    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
     prof_end(c, HGKS_K_FLUX_X + d);
     CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
     return HGKS_OK;
@@ -316,10 +367,15 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   for (int d = 0; d < 3; ++d) {
     if (p->n[d] < 5) return fail(nullptr, HGKS_EINVAL, "n[%d]=%d < 5", d, p->n[d]);
     if (!(p->hi[d] > p->lo[d])) return fail(nullptr, HGKS_EINVAL, "hi[%d] <= lo[%d]", d, d);
-    if (p->bc[d] != HGKS_PERIODIC) return fail(nullptr, HGKS_EINVAL, "only periodic boundaries are implemented");
+    if (p->bc[d] != HGKS_PERIODIC && p->bc[d] != HGKS_WALL_ISOTHERMAL) return fail(nullptr, HGKS_EINVAL, "bc[%d] invalid", d);
+    if (p->stretch[d] != HGKS_UNIFORM && p->stretch[d] != HGKS_TANH) return fail(nullptr, HGKS_EINVAL, "stretch[%d] invalid", d);
+    if (d == 2 && (p->bc[d] != HGKS_PERIODIC || p->stretch[d] != HGKS_UNIFORM))
+      return fail(nullptr, HGKS_EINVAL, "z is the slab axis: it must be periodic and uniform");
+    if (p->stretch[d] == HGKS_TANH && !(p->stretch_b[d] > 0.0)) return fail(nullptr, HGKS_EINVAL, "stretch_b[%d] must be > 0", d);
+    if (p->bc[d] == HGKS_WALL_ISOTHERMAL && !(p->T_wall > 0.0)) return fail(nullptr, HGKS_EINVAL, "T_wall must be > 0 with walls");
   }
   if (!(p->gamma > 1.0 && p->gamma <= 5.0 / 3.0 + 1e-12)) return fail(nullptr, HGKS_EINVAL, "gamma=%g outside (1, 5/3]", p->gamma);
-  if (p->prandtl != 1.0) return fail(nullptr, HGKS_EINVAL, "prandtl=%g: only Pr = 1 is implemented", p->prandtl);
+  if (!(p->prandtl > 0.0)) return fail(nullptr, HGKS_EINVAL, "prandtl=%g must be > 0", p->prandtl);
   if (!(p->mu_ref >= 0.0)) return fail(nullptr, HGKS_EINVAL, "mu_ref < 0");
   if (p->mu_law == HGKS_MU_POWER && !(p->T_ref > 0.0)) return fail(nullptr, HGKS_EINVAL, "T_ref must be > 0 for the power law");
   if (!(p->dt_fixed > 0.0) && !(p->cfl > 0.0)) return fail(nullptr, HGKS_EINVAL, "need cfl > 0 or dt_fixed > 0");
@@ -387,6 +443,31 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     ok = ok && cudaEventCreateWithFlags(&c->ev_flux[d], cudaEventDisableTiming) == cudaSuccess;
   }
   ok = ok && cudaMalloc(&c->stage64, 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double)) == cudaSuccess;
+  {  // metric tables of the three axes (local extents; z uses the global plane index)
+    const int nloc[3] = {c->n[0], c->n[1], c->nzl}, j0[3] = {0, 0, c->z0};
+    size_t tot = 0;
+    for (int d = 0; d < 3; ++d) {
+      c->metric_off[d][0] = tot;
+      c->metric_off[d][1] = tot + nloc[d] + 1;
+      c->metric_off[d][2] = tot + nloc[d] + 1 + 2 * nloc[d];
+      tot += (nloc[d] + 1) + 2 * nloc[d] + nloc[d];
+    }
+    double* h = (double*)malloc(tot * sizeof(double));
+    for (int d = 0; d < 3; ++d)
+      axis_tables(*p, d, p->n[d], j0[d], nloc[d], h + c->metric_off[d][0], h + c->metric_off[d][1], h + c->metric_off[d][2]);
+    ok = ok && cudaMalloc(&c->metric, tot * c->esz) == cudaSuccess;
+    if (ok) {
+      if (c->fp32) {
+        float* f = (float*)malloc(tot * sizeof(float));
+        for (size_t k = 0; k < tot; ++k) f[k] = (float)h[k];
+        ok = cudaMemcpy(c->metric, f, tot * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess;
+        free(f);
+      } else {
+        ok = cudaMemcpy(c->metric, h, tot * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+      }
+    }
+    free(h);
+  }
   ok = ok && cudaMalloc(&c->ctl, sizeof(Ctl)) == cudaSuccess;
   ok = ok && cudaMallocHost(&c->ctl_host, sizeof(Ctl)) == cudaSuccess;
   if (!ok) {
@@ -541,6 +622,7 @@ int hgks_destroy(hgks_ctx* c) {
   cudaFree(c->Qs);
   for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
   for (int b = 0; b < 2; ++b) cudaFree(c->FF[b]);
+  cudaFree(c->metric);
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   for (int d = 0; d < 3; ++d) {
@@ -587,9 +669,9 @@ int hgks_profile_read(hgks_ctx* c, double ms[HGKS_K_COUNT], int64_t launches[HGK
 }
 
 // ---- test entry points (include/hgks_test.h) --------------------------------------------------
-int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, double T_ref, double omega, double dt,
-                      const double* in, int64_t n, double* out) {
-  if (!in || !out || n < 0) return fail(nullptr, HGKS_EINVAL, "hgks_test_gp_flux: bad arguments");
+int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, double T_ref, double omega,
+                      double prandtl, double dt, const double* in, int64_t n, double* out) {
+  if (!in || !out || n < 0 || !(prandtl > 0)) return fail(nullptr, HGKS_EINVAL, "hgks_test_gp_flux: bad arguments");
   if (n == 0) return HGKS_OK;
   hgks_params p{};
   p.gamma = gamma;
@@ -602,8 +684,15 @@ int hgks_test_gp_flux(int precision, double gamma, int mu_law, double mu_ref, do
   CUDA_TRY(nullptr, cudaMalloc(&dout, 11 * n * sizeof(double)));
   CUDA_TRY(nullptr, cudaMemcpy(din, in, 55 * n * sizeof(double), cudaMemcpyHostToDevice));
   int blocks = (int)((n + 127) / 128);
-  if (precision == HGKS_FP32) gp_flux_test_kernel<float><<<blocks, 128>>>(din, dout, n, make_gas<float>(p), (float)dt);
-  else gp_flux_test_kernel<double><<<blocks, 128>>>(din, dout, n, make_gas<double>(p), dt);
+  p.prandtl = prandtl;
+  const bool prf = prandtl != 1.0;
+  if (precision == HGKS_FP32) {
+    if (prf) gp_flux_test_kernel<float, true><<<blocks, 128>>>(din, dout, n, make_gas<float>(p), (float)dt);
+    else gp_flux_test_kernel<float, false><<<blocks, 128>>>(din, dout, n, make_gas<float>(p), (float)dt);
+  } else {
+    if (prf) gp_flux_test_kernel<double, true><<<blocks, 128>>>(din, dout, n, make_gas<double>(p), dt);
+    else gp_flux_test_kernel<double, false><<<blocks, 128>>>(din, dout, n, make_gas<double>(p), dt);
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpy(out, dout, 11 * n * sizeof(double), cudaMemcpyDeviceToHost);
   cudaFree(din);

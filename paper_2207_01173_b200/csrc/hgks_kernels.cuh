@@ -36,10 +36,18 @@ struct Geo {
   int px, py;      // pitches: nx+6, ny+6
   long long plane; // 5*py*px: stride of one z plane
   long long vs;    // py*px: stride of one variable
-  T h[3];          // cell widths
-  T ih[3];         // 1/h
+  T h[3];          // cell widths of uniform axes
+  T ih[3];         // 1/h of uniform axes
   int z0;          // global z of local plane 0
   int ny_g, nx_g;  // global sizes (for linear cell ids)
+  // metric tables of every axis (local indices; O-18): J = d(cell index)/dx at the faces
+  // jf[d][0..n_d], at the Gauss abscissae jg[d][m * n_d + j] (m = 0: -sqrt(3)/6), and the
+  // reciprocal cell widths iw[d][0..n_d-1].  Uniform axes hold 1/h.
+  const T* jf[3];
+  const T* jg[3];
+  const T* iw[3];
+  int wall[3];     // 1: isothermal no-slip walls at both ends of the axis (O-17)
+  T T_wall;
 };
 
 template <typename T>
@@ -120,7 +128,7 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 1 + DIR : (c == 2 ? 1 + A1 : 1 + A2)));
   // cell -3 along the normal at (t1, t2)
   const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + t1 * s1 + t2 * s2;
-  const T ih = g.ih[DIR];
+  const T* jfn = g.jf[DIR];
   // every cell's WENO pair is evaluated at the same call site (the loop body), so all faces see
   // bitwise-identical arithmetic (uniform flow stays exactly uniform, O-P1)
   T s1v = p[0], s2v = p[sN], s3 = p[2 * sN], s4 = p[3 * sN], s5;
@@ -131,6 +139,7 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
     if (fn >= 0) {
+      const T ih = jfn[fn];  // metric of the face (O-18; 1/h on uniform axes)
       ff[L.at(0, c, fn, l)] = Bp;
       ff[L.at(1, c, fn, l)] = Ac;
       ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
 //      feeding the BGK flux (A4-A6); 4-point quadrature by warp shuffles (A7)
 // Lane layout in phase C: lane = 16 n + 8 m + a (a = t1 face in tile, (m, n) the Gauss point),
 // warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
-template <typename T, int DIR, int STAGE>
+template <typename T, int DIR, int STAGE, bool PRF>
 __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
   if (ctl->halt) return;
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   const int lane = threadIdx.x & 31;
   const int a = lane & 7, m = (lane >> 3) & 1, nn = lane >> 4;
   const int b = threadIdx.x >> 5;
-  const T ih1 = g.ih[A1], ih2 = g.ih[A2];
+  const T ih1 = g.jg[A1][m * n1 + min(t10 + a, n1 - 1)], ih2 = g.jg[A2][nn * n2 + min(t20 + b, n2 - 1)];
   const T sgn = nn ? T(-1) : T(1);
   // row r of this Gauss point's 5-row t2 stencil: rows b..b+4, mirrored for n = 1
   const T* row0 = sB + m * TT1 + a + (b + (nn ? 4 : 0)) * (5 * SB_RC);
@@ -269,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     return sgn * v;
   };
   const T dt = T(ctl->dt);
-  GpFlux<T, STAGE == 1> gf;
+  GpFlux<T, STAGE == 1, PRF> gf;
   {
     T Wl[5], Wr[5];
 #pragma unroll
@@ -327,7 +336,44 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   }
 }
 
-// ---- periodic ghosts along x and y over the interior z planes (A1; O-16) ----------------------
+// ---- ghost layers along x and y over the interior z planes (A1; O-16, O-17) ---------------------
+// 1. wall axes (isothermal no-slip mirror: U_g = -U_m, T_g = 2 T_wall - T_m, p_g = p_m, rho_g = p_g/T_g)
+//    over the interior of the other in-plane axis; 2. periodic axes over the full extended plane
+//    (a ghost cell copies the cell whose periodic coordinates are wrapped), which fills corners.
+template <typename T>
+__global__ void ghost_wall_kernel(T* __restrict__ q, Geo<T> g, double gamma, const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  const int nx = g.n[0], ny = g.n[1];
+  // items: (k, axis-position along the other in-plane axis, layer m, side); axes handled: x, y
+  for (int ax = 0; ax < 2; ++ax) {
+    if (!g.wall[ax]) continue;
+    const int n_ax = g.n[ax], n_ot = g.n[1 - ax];
+    const long long total = (long long)g.n[2] * n_ot * 3 * 2;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+      const int side = (int)(e % 2);
+      const int m = (int)((e / 2) % 3);
+      const int o = (int)((e / 6) % n_ot);
+      const int k = (int)(e / (6LL * n_ot));
+      const int im = side ? n_ax - 1 - m : m, ig = side ? n_ax + m : -1 - m;
+      int ci, cj, gi, gj;
+      if (ax == 0) { ci = im; gi = ig; cj = gj = o; } else { cj = im; gj = ig; ci = gi = o; }
+      const double rho = (double)q[qidx(g, 0, ci, cj, k)];
+      const double U = (double)q[qidx(g, 1, ci, cj, k)] / rho, V = (double)q[qidx(g, 2, ci, cj, k)] / rho,
+                   W = (double)q[qidx(g, 3, ci, cj, k)] / rho;
+      const double p = (gamma - 1.0) * ((double)q[qidx(g, 4, ci, cj, k)] - 0.5 * rho * (U * U + V * V + W * W));
+      const double Tg = 2.0 * (double)g.T_wall - p / rho;
+      const double rg = p / Tg;
+      q[qidx(g, 0, gi, gj, k)] = T(rg);
+      q[qidx(g, 1, gi, gj, k)] = T(-rg * U);
+      q[qidx(g, 2, gi, gj, k)] = T(-rg * V);
+      q[qidx(g, 3, gi, gj, k)] = T(-rg * W);
+      q[qidx(g, 4, gi, gj, k)] = T(p / (gamma - 1.0) + 0.5 * rg * (U * U + V * V + W * W));
+    }
+    (void)nx;
+    (void)ny;
+  }
+}
+
 template <typename T>
 __global__ void ghost_xy_kernel(T* __restrict__ q, Geo<T> g, const Ctl* __restrict__ ctl) {
   if (ctl->halt) return;
@@ -341,21 +387,24 @@ __global__ void ghost_xy_kernel(T* __restrict__ q, Geo<T> g, const Ctl* __restri
     const int v = (int)(r % 5);
     const int k = (int)(r / 5);
     const int i = ii - 3, j = jj - 3;
-    if (i >= 0 && i < nx && j >= 0 && j < ny) continue;
-    const int si = (i + nx) % nx, sj = (j + ny) % ny;  // n >= 5 > 3: one wrap suffices
+    // source: wrap the periodic in-plane axes only (wall ghosts come from ghost_wall_kernel)
+    const int si = g.wall[0] ? i : (i + nx) % nx, sj = g.wall[1] ? j : (j + ny) % ny;  // n >= 5 > 3
+    if (si == i && sj == j) continue;  // interior cell, or a pure wall ghost
     q[qidx(g, v, i, j, k)] = q[qidx(g, v, si, sj, k)];
   }
 }
 
 // max over d of (|U_d| + c)/dx_d for one cell (O-13); c = sqrt(gamma p / rho)
 template <typename T>
-__device__ __forceinline__ double wave_speed(const T (&c5)[5], const Geo<T>& g, double gamma, bool& ok) {
+__device__ __forceinline__ double wave_speed(const T (&c5)[5], const Geo<T>& g, int i, int j, int k, double gamma,
+                                             bool& ok) {
   double rho = (double)c5[0];
   double U = (double)c5[1] / rho, V = (double)c5[2] / rho, W = (double)c5[3] / rho;
   double p = (gamma - 1.0) * ((double)c5[4] - 0.5 * rho * (U * U + V * V + W * W));
   ok = (rho > 0.0) && (p > 0.0) && isfinite(rho) && isfinite(p) && isfinite(U) && isfinite(V) && isfinite(W);
   double c = sqrt(gamma * p / rho);
-  double sx = (fabs(U) + c) * (double)g.ih[0], sy = (fabs(V) + c) * (double)g.ih[1], sz = (fabs(W) + c) * (double)g.ih[2];
+  double sx = (fabs(U) + c) * (double)g.iw[0][i], sy = (fabs(V) + c) * (double)g.iw[1][j],
+         sz = (fabs(W) + c) * (double)g.iw[2][k];
   return fmax(sx, fmax(sy, sz));
 }
 
@@ -388,7 +437,7 @@ __global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __
     const long long iy = ((long long)k * (ny + 1) + j) * nx + i;
     const long long iz = ((long long)k * ny + j) * nx + i;
     const long long oy = nx, oz = (long long)nx * ny;
-    const T ihx = g.ih[0], ihy = g.ih[1], ihz = g.ih[2];
+    const T ihx = g.iw[0][i], ihy = g.iw[1][j], ihz = g.iw[2][k];
     const T tdt = T(dt);
     T out[5];
 #pragma unroll
@@ -411,7 +460,7 @@ __global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __
     }
     if (STAGE == 2) {
       bool ok;
-      smax = wave_speed(out, g, gamma, ok);
+      smax = wave_speed(out, g, i, j, k, gamma, ok);
       if (!ok) {
         smax = 0.0;
         unsigned long long gid = ((unsigned long long)(k + g.z0) * g.ny_g + j) * g.nx_g + i;
@@ -435,7 +484,7 @@ __global__ void cfl_kernel(const T* __restrict__ Q, Geo<T> g, double gamma, Ctl*
 #pragma unroll
     for (int c = 0; c < 5; ++c) c5[c] = Q[qidx(g, c, i, j, k)];
     bool ok;
-    double s = wave_speed(c5, g, gamma, ok);
+    double s = wave_speed(c5, g, i, j, k, gamma, ok);
     if (!ok) {
       unsigned long long gid = ((unsigned long long)(k + g.z0) * g.ny_g + j) * g.nx_g + i;
       atomicMin(&ctl->bad_cell, gid);
@@ -527,15 +576,15 @@ __global__ void operator_out_kernel(const T* __restrict__ FX, const T* __restric
   const long long iz = ((long long)k * ny + j) * nx + i;
   const long long oy = nx, oz = (long long)nx * ny;
   for (int c = 0; c < 10; ++c) {
-    const T v = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * g.ih[0] + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * g.ih[1] +
-                  (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * g.ih[2]);
+    const T v = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * g.iw[0][i] + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * g.iw[1][j] +
+                  (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * g.iw[2][k]);
     if (c < 5) L[c * ncell + e] = (double)v;
     else dL[(c - 5) * ncell + e] = (double)v;
   }
 }
 
 // batched Gauss-point flux (test entry hgks_test_gp_flux)
-template <typename T>
+template <typename T, bool PRF>
 __global__ void gp_flux_test_kernel(const double* __restrict__ in, double* __restrict__ out, long long n, GasK<T> gas, T dt) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -551,7 +600,7 @@ __global__ void gp_flux_test_kernel(const double* __restrict__ in, double* __res
     }
   }
   T F[5], dF[5], tau;
-  gp_flux<T, true>(gas, Wl, Wr, dWl, dWr, dW0, dt, F, dF, tau);
+  gp_flux<T, true, PRF>(gas, Wl, Wr, dWl, dWr, dW0, dt, F, dF, tau);
   double* o = out + 11 * e;
   for (int k = 0; k < 5; ++k) {
     o[k] = (double)F[k];

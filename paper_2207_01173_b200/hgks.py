@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("HGKS_LIB") or os.path.join(PKG, "libhgks.so")
 HGKS_OK, HGKS_EINVAL, HGKS_ECUDA, HGKS_ENCCL, HGKS_ESTATE, HGKS_ENOMEM = 0, -1, -2, -3, -4, -5
 HGKS_FP64, HGKS_FP32 = 0, 1
 HGKS_PERIODIC, HGKS_WALL_ISOTHERMAL = 0, 1
+HGKS_UNIFORM, HGKS_TANH = 0, 1
 HGKS_MU_CONST, HGKS_MU_POWER = 0, 1
 KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt", "recon")
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
@@ -38,9 +39,10 @@ class HgksError(RuntimeError):
 
 class Params(C.Structure):
     _fields_ = [("n", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
-                ("bc", C.c_int * 3), ("gamma", C.c_double), ("prandtl", C.c_double),
+                ("bc", C.c_int * 3), ("stretch", C.c_int * 3), ("stretch_b", C.c_double * 3),
+                ("gamma", C.c_double), ("prandtl", C.c_double),
                 ("mu_law", C.c_int), ("mu_ref", C.c_double), ("T_ref", C.c_double),
-                ("omega", C.c_double), ("cfl", C.c_double), ("dt_fixed", C.c_double),
+                ("omega", C.c_double), ("T_wall", C.c_double), ("cfl", C.c_double), ("dt_fixed", C.c_double),
                 ("precision", C.c_int), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("device", C.c_int32), ("nccl_id", C.c_void_p), ("stream", C.c_void_p)]
 
@@ -78,7 +80,7 @@ def lib():
         L.hgks_profile_enable.argtypes = [vp, C.c_int]
         L.hgks_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.hgks_test_gp_flux.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
-                                        C.c_double, C.c_double, _dp, C.c_int64, _dp]
+                                        C.c_double, C.c_double, C.c_double, _dp, C.c_int64, _dp]
         L.hgks_test_operator.argtypes = [vp, C.c_double, _dp, _dp]
         L.hgks_test_face_flux.argtypes = [vp, C.c_int, _dp]
         _lib = L
@@ -116,15 +118,18 @@ def hgks_get_nccl_id() -> bytes:
 
 def make_params(n, lo, hi, gamma=1.4, mu=0.0, prandtl=1.0, mu_law=HGKS_MU_CONST, T_ref=1.0,
                 omega=0.0, cfl=0.4, dt_fixed=0.0, precision=HGKS_FP64, rank=0, nranks=1,
-                device=0, nccl_id=None, stream=None, bc=(HGKS_PERIODIC,) * 3):
+                device=0, nccl_id=None, stream=None, bc=(HGKS_PERIODIC,) * 3,
+                stretch=(HGKS_UNIFORM,) * 3, stretch_b=(0.0, 0.0, 0.0), T_wall=1.0):
     p = Params()
     for d in range(3):
         p.n[d] = int(n[d])
         p.lo[d] = float(lo[d])
         p.hi[d] = float(hi[d])
         p.bc[d] = int(bc[d])
+        p.stretch[d] = int(stretch[d])
+        p.stretch_b[d] = float(stretch_b[d])
     p.gamma, p.prandtl, p.mu_law = gamma, prandtl, mu_law
-    p.mu_ref, p.T_ref, p.omega = mu, T_ref, omega
+    p.mu_ref, p.T_ref, p.omega, p.T_wall = mu, T_ref, omega, T_wall
     p.cfl, p.dt_fixed, p.precision = cfl, dt_fixed, precision
     p.rank, p.nranks, p.device = rank, nranks, device
     p._id_buf = C.create_string_buffer(nccl_id, len(nccl_id)) if nccl_id is not None else None
@@ -192,11 +197,11 @@ def hgks_profile_read(ctx):
 
 
 def hgks_test_gp_flux(records: np.ndarray, dt: float, gamma=1.4, mu=0.0, precision=HGKS_FP64,
-                      mu_law=HGKS_MU_CONST, T_ref=1.0, omega=0.0) -> np.ndarray:
+                      mu_law=HGKS_MU_CONST, T_ref=1.0, omega=0.0, prandtl=1.0) -> np.ndarray:
     """records [n,55] (Wl, Wr, dWl[3], dWr[3], dW0[3]) -> [n,11] (F, dF, tau)."""
     rec = np.ascontiguousarray(records, dtype=np.float64).reshape(-1, 55)
     out = np.zeros((rec.shape[0], 11))
-    _check(lib().hgks_test_gp_flux(precision, gamma, mu_law, mu, T_ref, omega, dt,
+    _check(lib().hgks_test_gp_flux(precision, gamma, mu_law, mu, T_ref, omega, prandtl, dt,
                                    rec.ctypes.data_as(_dp), rec.shape[0], out.ctypes.data_as(_dp)))
     return out
 

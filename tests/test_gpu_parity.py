@@ -59,7 +59,7 @@ def _random_records(n, seed, pscale=1.0, gscale=0.3):
     return rec
 
 
-def _oracle_records(rec, dt, mu, gas=None):
+def _oracle_records(rec, dt, mu, gas=None):  # noqa: D103
     gas = gas or O.make_gas(mu=mu)
     out = np.zeros((rec.shape[0], 11))
     for r in range(rec.shape[0]):
