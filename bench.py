@@ -151,6 +151,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hgks", choices=["hgks", "reference"])
     ap.add_argument("--n", type=int, default=256, help="TGV grid n^3 (BASELINE config 3: 256)")
+    ap.add_argument("--workload", default="tgv", choices=["tgv", "channel"],
+                    help="tgv: config 3 (headline); channel: config 4 (H2 128x256x128 unless --channel-grid)")
+    ap.add_argument("--channel-grid", default="128,256,128")
     ap.add_argument("--weak", action="store_true", help="weak scaling: n x n x (n/8 * N) per job")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--only-fp32", action="store_true", help="profiling aid: run only the fp32 leg")
@@ -175,6 +178,10 @@ def main():
     nz = (n // 8) * ws if args.weak else n
     grid = (n, n, nz)
     prm = inputs.tgv_params()
+    channel = args.workload == "channel"
+    if channel:
+        grid = tuple(int(x) for x in args.channel_grid.split(","))
+        chp = inputs.channel_params()
     nccl_id = None
     if ws > 1:
         obj = [H.hgks_get_nccl_id() if rank == 0 else None]
@@ -197,10 +204,19 @@ def main():
     lo, hi = (-math.pi,) * 3, (math.pi,) * 3  # weak mode: same box, nz = n/8 * N planes (anisotropic dz)
 
     def make_solver(precision):
+        if channel:  # config 4: walls in y, tanh mesh, power-law mu, Pr = 0.7
+            return H.Solver(grid, chp["lo"], chp["hi"], mu=chp["mu_w"], mu_law=H.HGKS_MU_POWER, T_ref=chp["T_w"],
+                            omega=chp["omega"], prandtl=chp["prandtl"], T_wall=chp["T_w"],
+                            bc=(H.HGKS_PERIODIC, H.HGKS_WALL_ISOTHERMAL, H.HGKS_PERIODIC),
+                            stretch=(H.HGKS_UNIFORM, H.HGKS_TANH, H.HGKS_UNIFORM), stretch_b=(0.0, chp["b_g"], 0.0),
+                            cfl=0.4, precision=precision, rank=rank, nranks=ws, device=local, nccl_id=nccl_id,
+                            stream=stream.cuda_stream)
         return H.Solver(grid, lo, hi, mu=prm["mu"], cfl=0.4, precision=precision, rank=rank, nranks=ws,
                         device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
 
     def local_field(s):
+        if channel:
+            return inputs.channel(grid, z_begin=s.z0, nz_local=s.nz_local)[0]
         # TGV on [-pi, pi]^3 with this rank's z planes
         q, _ = inputs.tgv(grid, z_begin=s.z0, nz_local=s.nz_local)
         return q
@@ -229,7 +245,7 @@ def main():
         ms_k, launches, total_launches = H.hgks_profile_read(s.ctx)
         H.hgks_profile_enable(s.ctx, False)
         ms = max_over_ranks(ms_local)
-        cells = n * n * nz
+        cells = grid[0] * grid[1] * grid[2]
         rate = cells * args.steps / (ms / 1000.0)
         res = dict(ms_per_step=ms / args.steps, value=rate, clocks=clk.summary(), ms_k=ms_k, launches=launches,
                    total_launches=total_launches, t=s.t)
@@ -270,7 +286,7 @@ def main():
     peaks = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tflops = N_SM * FP64_FMA_PER_CLK * 2 * sm_max * 1e6 / 1e12
-    cells_local = n * n * (nz // ws)
+    cells_local = grid[0] * grid[1] * grid[2] // ws
     roof = {"bound": "alu", "kernel": "flux_kernel<double,DIR,STAGE> (x,y,z faces, both stages)",
             "peak": peak_tflops, "unit": "TFLOP/s",
             "peak_source": f"derived: {N_SM} SMs x {FP64_FMA_PER_CLK} FP64 FMA/clk x 2 x {sm_max:.0f} MHz (DESIGN.md)",
@@ -278,7 +294,8 @@ def main():
             "avg_launch_ms": flux_ms / flux_launches if flux_launches else None, "traffic": None}
     if ftab:
         # executed FP64 flops per face per stage (ncu SASS count, profiles/flux_flops.json)
-        faces = 3 * cells_local + 3 * n * n  # all x,y,z faces of one rank's slab (approx +1 plane per dir)
+        gx, gy, gzl = grid[0], grid[1], grid[2] // ws
+        faces = 3 * cells_local + gy * gzl + gx * gzl + gx * gy  # x, y, z faces of one rank's slab
         flops_step = faces * (ftab["flop_per_face_stage1"] + ftab["flop_per_face_stage2"])
         achieved = flops_step * args.steps / (flux_ms / 1000.0) / 1e12
         roof.update(achieved=achieved, frac=achieved / peak_tflops, flop_source=ftab.get("source"),
@@ -289,9 +306,10 @@ def main():
         "metric": METRIC, "value": r64["value"], "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r64["ms_per_step"], "higher_is_better": True,
         "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"tgv{n}" + ("_weak" if args.weak else ""), "grid": list(grid), "precision": "fp64",
+        "config": {"workload": ("channel_" + "x".join(map(str, grid))) if channel else (f"tgv{n}" + ("_weak" if args.weak else "")),
+                   "grid": list(grid), "precision": "fp64",
                    "mode": "cfl 0.4 (dt allreduce each step)", "decomposition": f"z-slab x{ws}",
-                   "l2": "inputs larger than L2 (one state = %d MB)" % (5 * n * n * nz * 8 // 2**20)},
+                   "l2": "inputs larger than L2 (one state = %d MB)" % (5 * grid[0] * grid[1] * grid[2] * 8 // 2**20)},
         "clocks": clk,
         "gpu_launches": int(r64["total_launches"]),
         "roofline": roof,
@@ -306,7 +324,7 @@ def main():
         r32 = results["fp32"]
         line["fp32"] = {"value": r32["value"], "ms_per_step": r32["ms_per_step"], "clocks": r32["clocks"],
                         "e2e": r32.get("e2e"), "speedup_vs_fp64": r32["value"] / r64["value"]}
-    if not args.no_cpu:
+    if not args.no_cpu and not channel:
         v, cores, sec, sample = cpu_baseline(n, args.cpu_planes, prm["mu"], (2 * math.pi / n,) * 3)
         line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
                                 "sample": sample, "seconds": sec}

@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            *["-D" + d for d in defines], "-I", INCLUDE, "-I", inc, "-o", out, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
-           "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir]
+           "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir] + (["-rdc=false"] if False else [])
     subprocess.check_call(cmd)
     return out
 

@@ -20,6 +20,18 @@
 
 using namespace hgks;
 
+#ifdef HGKS_PHASE_TIMING
+extern "C" int hgks_debug_phase_cycles(unsigned long long out[4], int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
 namespace {
 
 thread_local std::string g_thread_err;
@@ -256,7 +268,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   auto flux = [&](int d) -> int {
     T* ff = (T*)c->FF[d & 1];
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, n3[d] + 1);
+    dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, (n3[d] + 1 + HGKS_FLUX_TPB - 1) / HGKS_FLUX_TPB);
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
     const bool prf = c->p.prandtl != 1.0;

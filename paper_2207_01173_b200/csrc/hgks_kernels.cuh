@@ -15,6 +15,9 @@
 #pragma once
 #include "gks_device.cuh"
 
+#ifdef HGKS_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[4];  // debug builds: cycles per flux phase
+#endif
 namespace hgks {
 
 // device control block (one per context)
@@ -55,6 +58,9 @@ __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, 
   return (long long)(k + 3) * g.plane + (long long)v * g.vs + (long long)(j + 3) * g.px + (i + 3);
 }
 
+#ifndef HGKS_FLUX_TPB
+#define HGKS_FLUX_TPB 2  // consecutive normal faces per flux block (face-field prefetch depth)
+#endif
 #ifndef HGKS_FLUX_MINB
 #define HGKS_FLUX_MINB 2  // resident flux blocks per SM (register budget 128/thread)
 #endif
@@ -174,11 +180,12 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   T* sB = sA + 6 * 5 * SA_C;               // [TL2][5][SB_RC]
 
   const int n1 = g.n[A1], n2 = g.n[A2];
-  const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2, fn = blockIdx.z;  // face fn: cells fn-1 | fn
-  // ---- phase A: tile of face fields (6 x 5 x TL1 x TL2) from the reconstruction array -------
-  // asynchronous global->shared copies (cp.async / LDGSTS): each thread owns one tile line
-  // (l1, l2) and copies its 30 (field, component) values, all in flight at once
-  {
+  const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2;
+  // HGKS_FLUX_TPB consecutive normal faces per block: the face fields of face fn+1 are copied
+  // (cp.async) into sA while face fn is in phase C, so only the first copy's latency is exposed
+  const int fn0 = blockIdx.z * HGKS_FLUX_TPB;
+  const int nfn = min(HGKS_FLUX_TPB, g.n[DIR] + 1 - fn0);
+  auto issue_A = [&](int fn) {
     const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
     const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sA);
@@ -210,9 +217,22 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
         }
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue_A(fn0);
+#ifdef HGKS_PHASE_TIMING
+  long long tA = 0, tB = 0, tC = 0;
+#endif
+  for (int it = 0; it < nfn; ++it) {
+    const int fn = fn0 + it;  // face fn: cells fn-1 | fn
+#ifdef HGKS_PHASE_TIMING
+    long long tp0 = clock64();
+#endif
     asm volatile("cp.async.wait_all;" ::: "memory");
-  }
-  __syncthreads();
+    __syncthreads();  // sA(fn) landed; every thread is done with sB of the previous face
+#ifdef HGKS_PHASE_TIMING
+    long long tp1 = clock64();
+#endif
 
   // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
   // One item = (a, c, l2) computes both Gauss abscissae m = 0, 1 from the same 30 loads: point
@@ -249,7 +269,11 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
       dst[k * SB_K + TT1] = o1[k];
     }
   }
-  __syncthreads();
+  __syncthreads();  // sB complete; sA free for the next face
+  if (it + 1 < nfn) issue_A(fn + 1);
+#ifdef HGKS_PHASE_TIMING
+  long long tp2 = clock64();
+#endif
 
   // ---- phase C: one thread per Gauss point ----------------------------------------------------
   const int lane = threadIdx.x & 31;
@@ -334,6 +358,21 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
       flux[(5 + gc[k]) * nface + id] = T(0.25) * dF[k];
     }
   }
+#ifdef HGKS_PHASE_TIMING
+  long long tp3 = clock64();
+  tA += tp1 - tp0;
+  tB += tp2 - tp1;
+  tC += tp3 - tp2;
+#endif
+  }  // faces of this block
+#ifdef HGKS_PHASE_TIMING
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_phase_cycles[0], (unsigned long long)tA);
+    atomicAdd(&g_phase_cycles[1], (unsigned long long)tB);
+    atomicAdd(&g_phase_cycles[2], (unsigned long long)tC);
+    atomicAdd(&g_phase_cycles[3], (unsigned long long)nfn);
+  }
+#endif
 }
 
 // ---- ghost layers along x and y over the interior z planes (A1; O-16, O-17) ---------------------
