@@ -281,25 +281,36 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   const int b = threadIdx.x >> 5;
   const T ih1 = g.jg[A1][m * n1 + min(t10 + a, n1 - 1)], ih2 = g.jg[A2][nn * n2 + min(t20 + b, n2 - 1)];
   const T sgn = nn ? T(-1) : T(1);
-  // row r of this Gauss point's 5-row t2 stencil: rows b..b+4, mirrored for n = 1
-  const T* row0 = sB + m * TT1 + a + (b + (nn ? 4 : 0)) * (5 * SB_RC);
-  const int rstep = nn ? -5 * SB_RC : 5 * SB_RC;
-  // t2 pass of slot k, component c: value (wv) or derivative (wd).  The empty asm with a memory
-  // clobber keeps ptxas from hoisting these shared loads ahead of earlier flux work (register
-  // pressure: they would be spilled).
+  // t2 pass of slot k, component c, over rows b..b+4: value (wv) or derivative (wd) at this Gauss
+  // point.  n = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r]:
+  //  * fp64: mirror the ROW order instead (weights stay immediates); lanes n = 0 / 1 sit in different
+  //    half-warps, so the two row streams never share a bank within a 128-byte wavefront;
+  //  * fp32: a whole warp is one wavefront, so keep the row order (n = 0 and n = 1 lanes read the
+  //    same word: broadcast) and hold the 10 mirrored weights in registers.
+  // The empty asm with a memory clobber keeps ptxas from hoisting these shared loads ahead of
+  // earlier flux work (register pressure: they would be spilled).
+  constexpr bool kRowMirror = sizeof(T) == 8;
+  const T* row0 = sB + m * TT1 + a + (b + (kRowMirror && nn ? 4 : 0)) * (5 * SB_RC);
+  const int rstep = (kRowMirror && nn) ? -5 * SB_RC : 5 * SB_RC;
+  T wvl[5], wdl[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    wvl[r] = (!kRowMirror && nn) ? T(kWV0(4 - r)) : T(kWV0(r));
+    wdl[r] = (!kRowMirror && nn) ? -T(kWD0(4 - r)) : T(kWD0(r));
+  }
   auto tv = [&](int c, int k) {
     asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += T(kWV0(r)) * row0[r * rstep + c * SB_RC + k * SB_K];
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? T(kWV0(r)) : wvl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
     return v;
   };
   auto td = [&](int c, int k) {
     asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += T(kWD0(r)) * row0[r * rstep + c * SB_RC + k * SB_K];
-    return sgn * v;
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? T(kWD0(r)) : wdl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
+    return kRowMirror ? sgn * v : v;
   };
   const T dt = T(ctl->dt);
   GpFlux<T, STAGE == 1, PRF> gf;
