@@ -25,6 +25,8 @@ namespace hgks {
 // ---------------------------------------------------------------------------------------------
 __host__ __device__ __forceinline__ double m_sqrt(double x) { return sqrt(x); }
 __host__ __device__ __forceinline__ float m_sqrt(float x) { return sqrtf(x); }
+__host__ __device__ __forceinline__ double m_rsqrt(double x) { return rsqrt(x); }
+__host__ __device__ __forceinline__ float m_rsqrt(float x) { return rsqrtf(x); }
 __host__ __device__ __forceinline__ double m_exp(double x) { return exp(x); }
 __host__ __device__ __forceinline__ float m_exp(float x) { return expf(x); }
 __host__ __device__ __forceinline__ double m_erfc(double x) { return erfc(x); }
@@ -100,6 +102,7 @@ struct GasK {
   T mu_ref, T_ref, omega;
   int mu_law;  // 0 const, 1 power law
   T prf;       // 1/Pr - 1 (heat-flux fix, O-12; used by GpFlux<.., PRF = true>)
+  T ik3;       // 1/(K+3), host-computed
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -213,13 +216,15 @@ HD void shift_vec(T su, T sv, T sw, T (&x)[5]) {
 // One direction of the compatibility solves of one Maxwellian in its fully co-moving
 // frame: from the conservative derivative dW along local axis I, the spatial slope a_I
 // (<a_I> = dW_I / rho, O-7) and the contribution s_I b_c + Q_I(a_I) to
-// R = sum_i <u_i a_i.psi psi> (frame components), whose negative is M A.
+// R = sum_i <u_i a_i.psi psi> (frame components), whose negative is M A.  Everything here is
+// linear in dW, so the 1/rho of O-7 is left out: the slopes come out scaled by rho, which is exactly
+// the factor rho of every slope term of the flux (callers scale only the Z term by rho).
 template <int I, typename T>
-HD void slope_dir(T K, T irho, T U, T V, T W, T th, T it, const T (&dW)[5], T (&a)[5], T (&R)[5]) {
+HD void slope_dir(T K, T ik3, T U, T V, T W, T th, T it, const T (&dW)[5], T (&a)[5], T (&R)[5]) {
   const T hK3 = T(0.5) * (K + T(3)) * th;
-  const T c5 = T(2) * it * it * rcp(K + T(3));
+  const T c5 = T(2) * it * it * ik3;
   const T hK5t = T(0.5) * (K + T(5)) * th;
-  const T b1 = dW[0] * irho, b2 = dW[1] * irho, b3 = dW[2] * irho, b4 = dW[3] * irho, b5 = dW[4] * irho;
+  const T b1 = dW[0], b2 = dW[1], b3 = dW[2], b4 = dW[3], b5 = dW[4];
   // b_c = T(-s) b
   const T c5v = b5 - U * b2 - V * b3 - W * b4 + T(0.5) * (U * U + V * V + W * W) * b1;
   const T c2 = b2 - U * b1, c3 = b3 - V * b1, c4 = b4 - W * b1;
@@ -240,9 +245,9 @@ HD void slope_dir(T K, T irho, T U, T V, T W, T th, T it, const T (&dW)[5], T (&
 
 // temporal slope A = M^-1 (-R) in the co-moving frame
 template <typename T>
-HD void temporal_slope(T K, T th, T it, const T (&R)[5], T (&A)[5]) {
+HD void temporal_slope(T K, T ik3, T th, T it, const T (&R)[5], T (&A)[5]) {
   const T hK3 = T(0.5) * (K + T(3)) * th;
-  const T c5 = T(2) * it * it * rcp(K + T(3));
+  const T c5 = T(2) * it * it * ik3;
   const T r1 = -R[0];
   A[4] = c5 * (-R[4] - hK3 * r1);
   A[0] = r1 - hK3 * A[4];
@@ -265,7 +270,7 @@ struct GpFlux {
   T rl, irl, Ul, Vl, Wl, thl, hl0, hl1;
   T rr, irr, Ur, Vr, Wr, thr, hr0, hr1;
   T r0, ir0, U0, V0, W0, th0;
-  T h, idt, dt, prf;
+  T h, idt, dt, prf, ik3;
   T F[5], dF[5], tau;
 
   HD void begin(const GasK<T>& g, const T (&WL)[5], const T (&WR)[5], T dt_, T idt_) {
@@ -273,8 +278,9 @@ struct GpFlux {
     dt = dt_;
     idt = idt_;
     prf = g.prf;
+    ik3 = g.ik3;
     const T isqpi = T(0.56418958354775628694807945156077);  // 1/sqrt(pi)
-    const T k3 = T(4) * rcp(K + T(3));
+    const T k3 = T(4) * ik3;
     rl = WL[0];
     irl = rcp(rl);
     Ul = WL[1] * irl;
@@ -288,12 +294,12 @@ struct GpFlux {
     Vr = WR[2] * irr;
     Wr = WR[3] * irr;
     thr = T(0.5) * k3 * (WR[4] * irr - T(0.5) * (Ur * Ur + Vr * Vr + Wr * Wr));
-    // half-space seeds (A.2): sqrt(lambda) = sqrt(1/(2 theta))
-    const T sl = m_sqrt(T(0.5) * rcp(thl)), sr = m_sqrt(T(0.5) * rcp(thr));
+    // half-space seeds (A.2): sqrt(lambda) = rsqrt(2 theta), 1/sqrt(lambda) = 2 theta rsqrt(2 theta)
+    const T sl = m_rsqrt(T(2) * thl), sr = m_rsqrt(T(2) * thr);
     hl0 = half_erfc(-sl * Ul);
-    hl1 = Ul * hl0 + T(0.5) * isqpi * m_exp(-sl * sl * Ul * Ul) * rcp(sl);
+    hl1 = Ul * hl0 + isqpi * thl * sl * m_exp(-sl * sl * Ul * Ul);
     hr0 = half_erfc(sr * Ur);
-    hr1 = Ur * hr0 - T(0.5) * isqpi * m_exp(-sr * sr * Ur * Ur) * rcp(sr);
+    hr1 = Ur * hr0 - isqpi * thr * sr * m_exp(-sr * sr * Ur * Ur);
     // Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
     const T hl2 = Ul * hl1 + thl * hl0, hr2 = Ur * hr1 + thr * hr0;
     const T q0 = rl * hl0 + rr * hr0;
@@ -312,7 +318,9 @@ struct GpFlux {
     const T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
     tau = qdiv(mu * ir0, th0);
     // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
-    h = tau > T(0) ? m_exp(-T(0.5) * dt * rcp(tau)) : T(0);
+    // (below 1e-20 -- dt/tau > 92, e.g. every low-Mach TGV face -- h changes no Gamma above rounding)
+    const T harg = -T(0.5) * dt * rcp(tau);
+    h = (tau > T(0) && harg > T(-46)) ? m_exp(harg) : T(0);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       F[k] = T(0);
@@ -345,22 +353,25 @@ struct GpFlux {
     }
   }
 
+  // F += T(s)(rho ga Z + gb X + gc Y), dF likewise with Gamma' (X, Y already carry rho)
   HD void accumulate(bool eq, T rho, T su, T sv, T sw, const T (&Z)[5], const T (&X)[5], const T (&Y)[5]) {
     T ga, gb, gc, gpa, gpb, gpc;
     gammas(eq, ga, gb, gc, gpa, gpb, gpc);
+    const T rpa = rho * gpa;
     T d[5];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) d[k] = gpa * Z[k] + gpb * X[k] + gpc * Y[k];
+    for (int k = 0; k < 5; ++k) d[k] = rpa * Z[k] + gpb * X[k] + gpc * Y[k];
     shift_vec(su, sv, sw, d);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) dF[k] += rho * d[k];
+    for (int k = 0; k < 5; ++k) dF[k] += d[k];
     if (NEED_F) {
+      const T ra = rho * ga;
       T f[5];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) f[k] = ga * Z[k] + gb * X[k] + gc * Y[k];
+      for (int k = 0; k < 5; ++k) f[k] = ra * Z[k] + gb * X[k] + gc * Y[k];
       shift_vec(su, sv, sw, f);
 #pragma unroll
-      for (int k = 0; k < 5; ++k) F[k] += rho * f[k];
+      for (int k = 0; k < 5; ++k) F[k] += f[k];
     }
   }
 
@@ -379,9 +390,9 @@ struct GpFlux {
     for (int i = 0; i < 3; ++i) {
       T dW[5], a[5];
       load(i, dW);
-      if (i == 0) slope_dir<0>(K, ir0, U0, V0, W0, th, it, dW, a, R);
-      if (i == 1) slope_dir<1>(K, ir0, U0, V0, W0, th, it, dW, a, R);
-      if (i == 2) slope_dir<2>(K, ir0, U0, V0, W0, th, it, dW, a, R);
+      if (i == 0) slope_dir<0>(K, ik3, U0, V0, W0, th, it, dW, a, R);
+      if (i == 1) slope_dir<1>(K, ik3, U0, V0, W0, th, it, dW, a, R);
+      if (i == 2) slope_dir<2>(K, ik3, U0, V0, W0, th, it, dW, a, R);
       const T si = i == 0 ? U0 : (i == 1 ? V0 : W0);
       // s_i Q_x(a)
       X[0] += si * th * a[1];
@@ -402,7 +413,7 @@ struct GpFlux {
       }
     }
     T A[5];
-    temporal_slope(K, th, it, R, A);
+    temporal_slope(K, ik3, th, it, R, A);
     T Y[5];
     Y[0] = -U0 * R[0] + th * A[1];
     Y[1] = -U0 * R[1] + th * (A[0] + hK5t * A[4]);
@@ -413,8 +424,8 @@ struct GpFlux {
       const T qx = X[4], qy = Y[4] + U0 * R[4];  // X[4] before the U0 R shift = X_c[4] - U0 R[4]
       T ga, gb, gc, gpa, gpb, gpc;
       gammas(true, ga, gb, gc, gpa, gpb, gpc);
-      dF[4] += r0 * prf * (gpb * qx + gpc * qy);
-      if (NEED_F) F[4] += r0 * prf * (gb * qx + gc * qy);
+      dF[4] += prf * (gpb * qx + gpc * qy);
+      if (NEED_F) F[4] += prf * (gb * qx + gc * qy);
     }
 #pragma unroll
     for (int k = 0; k < 5; ++k) X[k] += U0 * R[k];
@@ -426,7 +437,7 @@ struct GpFlux {
   // with the tangential velocity (V, W) only.
   template <int SIDE, class Load>
   HD void add_side(Load&& load) {
-    const T rho = SIDE > 0 ? rl : rr, irho = SIDE > 0 ? irl : irr;
+    const T rho = SIDE > 0 ? rl : rr;
     const T U = SIDE > 0 ? Ul : Ur, V = SIDE > 0 ? Vl : Vr, W = SIDE > 0 ? Wl : Wr;
     const T th = SIDE > 0 ? thl : thr, it = rcp(th);
     // half-space u-moments t_0..t_6 (A.2 recursion)
@@ -460,9 +471,9 @@ struct GpFlux {
     for (int i = 0; i < 3; ++i) {
       T dW[5], a[5];
       load(i, dW);
-      if (i == 0) slope_dir<0>(K, irho, U, V, W, th, it, dW, a, R);
-      if (i == 1) slope_dir<1>(K, irho, U, V, W, th, it, dW, a, R);
-      if (i == 2) slope_dir<2>(K, irho, U, V, W, th, it, dW, a, R);
+      if (i == 0) slope_dir<0>(K, ik3, U, V, W, th, it, dW, a, R);
+      if (i == 1) slope_dir<1>(K, ik3, U, V, W, th, it, dW, a, R);
+      if (i == 2) slope_dir<2>(K, ik3, U, V, W, th, it, dW, a, R);
       to_t(a);
       if (PRF) {
 #pragma unroll
@@ -485,7 +496,7 @@ struct GpFlux {
       }
     }
     T A[5];
-    temporal_slope(K, th, it, R, A);
+    temporal_slope(K, ik3, th, it, R, A);
     to_t(A);
     T Y[5] = {T(0), T(0), T(0), T(0), T(0)};
     H(A, 1, T(1), Y);
@@ -510,17 +521,17 @@ struct GpFlux {
       auto heat = [&](T a, T b, T c) {
         T Fv[5], Wv[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-          Fv[k] = a * Z[k] + b * X[k] + c * Y[k];
-          Wv[k] = a * Zd[k] + b * Xd[k] + c * Yd[k];
+        for (int k = 0; k < 5; ++k) {  // X, Y, Xd, Yd carry rho (slopes scaled by rho)
+          Fv[k] = rho * a * Z[k] + b * X[k] + c * Y[k];
+          Wv[k] = rho * a * Zd[k] + b * Xd[k] + c * Yd[k];
         }
         return Fv[4] - (dx * Fv[1] + dy * Fv[2] + dz * Fv[3]) + d2 * Fv[0] -
                dx * (Wv[4] - (dx * Wv[1] + dy * Wv[2] + dz * Wv[3]) + d2 * Wv[0]);
       };
       T ga, gb, gc, gpa, gpb, gpc;
       gammas(false, ga, gb, gc, gpa, gpb, gpc);
-      dF[4] += rho * prf * heat(gpa, gpb, gpc);
-      if (NEED_F) F[4] += rho * prf * heat(ga, gb, gc);
+      dF[4] += prf * heat(gpa, gpb, gpc);
+      if (NEED_F) F[4] += prf * heat(ga, gb, gc);
     }
     accumulate(false, rho, T(0), V, W, Z, X, Y);
   }

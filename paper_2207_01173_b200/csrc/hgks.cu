@@ -190,6 +190,7 @@ static GasK<T> make_gas(const hgks_params& p) {
   g.omega = T(p.omega);
   g.mu_law = (int)p.mu_law;
   g.prf = T(1.0 / p.prandtl - 1.0);
+  g.ik3 = T(1.0 / ((5.0 - 3.0 * p.gamma) / (p.gamma - 1.0) + 3.0));
   return g;
 }
 

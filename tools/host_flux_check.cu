@@ -8,6 +8,7 @@ extern "C" void host_gp_flux(const double* in, long n, double gamma, double mu, 
   g.K = (5.0 - 3.0 * gamma) / (gamma - 1.0);
   g.gamma = gamma; g.mu_ref = mu; g.T_ref = T_ref; g.omega = omega; g.mu_law = mu_law;
   g.prf = 1.0 / prandtl - 1.0;
+  g.ik3 = 1.0 / (g.K + 3.0);
   for (long e = 0; e < n; ++e) {
     const double* r = in + 55 * e;
     double Wl[5], Wr[5], dWl[3][5], dWr[3][5], dW0[3][5];
