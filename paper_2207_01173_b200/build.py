@@ -32,6 +32,8 @@ def sources():
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
     srcs = sources()
     out = out or LIB
+    if os.sep not in out:  # bare file name: a variant next to the default library
+        out = os.path.join(os.path.dirname(LIB), out)
     if not force and os.path.exists(out) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
         return out
     inc, nccl_so, nccl_dir = _nccl_dirs()

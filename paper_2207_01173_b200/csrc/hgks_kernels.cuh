@@ -64,7 +64,10 @@ __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, 
 #ifndef HGKS_FLUX_MINB
 #define HGKS_FLUX_MINB 2  // resident flux blocks per SM (register budget 128/thread)
 #endif
-constexpr int TT1 = 8, TT2 = 8;            // faces per tile along t1, t2
+#ifndef HGKS_TT2
+#define HGKS_TT2 8
+#endif
+constexpr int TT1 = 8, TT2 = HGKS_TT2;      // faces per tile along t1, t2
 constexpr int TL1 = TT1 + 4, TL2 = TT2 + 4;  // lines per tile (+-2 tangential halo)
 constexpr int NTHREADS_FLUX = TT1 * TT2 * 4;
 constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
@@ -289,7 +292,10 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   //    same word: broadcast) and hold the 10 mirrored weights in registers.
   // The empty asm with a memory clobber keeps ptxas from hoisting these shared loads ahead of
   // earlier flux work (register pressure: they would be spilled).
-  constexpr bool kRowMirror = sizeof(T) == 8;
+#ifndef HGKS_ROW_MIRROR64
+#define HGKS_ROW_MIRROR64 1
+#endif
+  constexpr bool kRowMirror = sizeof(T) == 8 && HGKS_ROW_MIRROR64;
   const T* row0 = sB + m * TT1 + a + (b + (kRowMirror && nn ? 4 : 0)) * (5 * SB_RC);
   const int rstep = (kRowMirror && nn) ? -5 * SB_RC : 5 * SB_RC;
   T wvl[5], wdl[5];
@@ -314,24 +320,37 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   };
   const T dt = T(ctl->dt);
   GpFlux<T, STAGE == 1, PRF> gf;
+  // value and t2-derivative of Ql, Qr from the same five row loads (the t2 derivatives are held
+  // until the side passes: 10 more live registers, 50 fewer shared loads per Gauss point)
+  auto tvd = [&](int c, int k, T& v, T& d) {
+    asm volatile("" ::: "memory");
+    v = T(0);
+    d = T(0);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const T x = row0[r * rstep + c * SB_RC + k * SB_K];
+      v += (kRowMirror ? T(kWV0(r)) : wvl[r]) * x;
+      d += (kRowMirror ? T(kWD0(r)) : wdl[r]) * x;
+    }
+    if (kRowMirror) d *= sgn;
+  };
+  T d2l[5], d2r[5];
   {
     T Wl[5], Wr[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      Wl[c] = tv(c, 0);
-      Wr[c] = tv(c, 1);
+      tvd(c, 0, Wl[c], d2l[c]);
+      tvd(c, 1, Wr[c], d2r[c]);
     }
     gf.begin(gas, Wl, Wr, dt, T(1) / dt);
   }
-  // derivative inputs, one direction at a time: normal (value of dQ/dn or D), t1 (D1 slots),
-  // t2 (t2-derivative of Ql, Qr or C)
   gf.template add_side<+1>([&](int i, T (&d)[5]) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 2) : (i == 1 ? tv(c, 6) * ih1 : td(c, 0) * ih2);
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 2) : (i == 1 ? tv(c, 6) * ih1 : d2l[c] * ih2);
   });
   gf.template add_side<-1>([&](int i, T (&d)[5]) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 3) : (i == 1 ? tv(c, 7) * ih1 : td(c, 1) * ih2);
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 3) : (i == 1 ? tv(c, 7) * ih1 : d2r[c] * ih2);
   });
   gf.add_equilibrium([&](int i, T (&d)[5]) {
 #pragma unroll

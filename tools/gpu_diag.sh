@@ -1,1 +1,1 @@
-./tools/microbench/fp64_pipes; nvidia-smi --query-gpu=clocks.sm --format=csv
+bash tools/gpu_variants.sh libhgks.so libhgks_t16.so
