@@ -36,23 +36,26 @@ __host__ __device__ __forceinline__ double m_erfc(double x) { return erfc(x); }
 // erfc(x)/2.  For |x| < 0.75 (every low-Mach state: x = sqrt(lambda) U) the Maclaurin series of
 // erf (14 terms, truncation < 1e-19; measured max relative error 8e-16 for erfc(-x)/2, 2e-15 for
 // erfc(x)/2 at x = 0.75) replaces the general-range libdevice erfc (~145 instructions).
+// 64-bit constants live in constant memory on the device: DFMA takes a c[][] operand directly,
+// while a 64-bit literal costs two uniform-register moves (UMOV) at every use.
+#define HGKS_ERFC_COEFS -5.9477940136376354e-12, 8.35070279514724e-11, -1.0892221037148573e-09, 1.3122532963802806e-08, -1.4503852223150468e-07, 1.4589169000933706e-06, -1.3227513227513228e-05, 0.00010683760683760684, -0.0007575757575757576, 0.004629629629629629, -0.023809523809523808, 0.1, -0.3333333333333333, 1.0
+#ifdef __CUDACC__
+__constant__ double c_erfc_series[14] = {HGKS_ERFC_COEFS};
+#endif
+__host__ __device__ __forceinline__ double erfc_series_coef(int i) {
+#ifdef __CUDA_ARCH__
+  return c_erfc_series[i];
+#else
+  constexpr double k[14] = {HGKS_ERFC_COEFS};
+  return k[i];
+#endif
+}
 __host__ __device__ __forceinline__ double half_erfc(double x) {
   if (HGKS_FAST_ERFC && fabs(x) < 0.75) {
     const double z = x * x;
-    double s = -5.9477940136376354e-12;
-    s = fma(s, z, 8.35070279514724e-11);
-    s = fma(s, z, -1.0892221037148573e-09);
-    s = fma(s, z, 1.3122532963802806e-08);
-    s = fma(s, z, -1.4503852223150468e-07);
-    s = fma(s, z, 1.4589169000933706e-06);
-    s = fma(s, z, -1.3227513227513228e-05);
-    s = fma(s, z, 0.00010683760683760684);
-    s = fma(s, z, -0.0007575757575757576);
-    s = fma(s, z, 0.004629629629629629);
-    s = fma(s, z, -0.023809523809523808);
-    s = fma(s, z, 0.1);
-    s = fma(s, z, -0.3333333333333333);
-    s = fma(s, z, 1.0);
+    double s = erfc_series_coef(0);
+#pragma unroll
+    for (int i = 1; i < 14; ++i) s = fma(s, z, erfc_series_coef(i));
     return fma(-0.56418958354775628694807945156077 * x, s, 0.5);  // 1/2 - x s / sqrt(pi)
   }
   return 0.5 * erfc(x);
@@ -183,6 +186,21 @@ __host__ __device__ constexpr double kWD0(int r) {
        : r == 3 ? 2.0 / 3.0 - 13.0 * HGKS_S3 / 54.0
                 : -1.0 / 12.0 + HGKS_S3 / 54.0;
 }
+
+// the quartic Gauss-point weights as device operands: constant memory for fp64 (see c_erfc_series),
+// 32-bit literals for fp32
+#ifdef __CUDACC__
+__constant__ double c_wv0[5] = {kWV0(0), kWV0(1), kWV0(2), kWV0(3), kWV0(4)};
+__constant__ double c_wd0[5] = {kWD0(0), kWD0(1), kWD0(2), kWD0(3), kWD0(4)};
+template <class T>
+__device__ __forceinline__ T wv0(int r) { return T(kWV0(r)); }
+template <class T>
+__device__ __forceinline__ T wd0(int r) { return T(kWD0(r)); }
+template <>
+__device__ __forceinline__ double wv0<double>(int r) { return c_wv0[r]; }
+template <>
+__device__ __forceinline__ double wd0<double>(int r) { return c_wd0[r]; }
+#endif
 
 // ---------------------------------------------------------------------------------------------
 // Kinetic part (A4-A6).  Every Maxwellian is handled in a frame moving with it, where its

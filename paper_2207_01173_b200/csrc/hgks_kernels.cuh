@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     const T* src = sA + c * SA_C + l2 * TL1 + a;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const T wv0 = T(kWV0(r)), wd0 = T(kWD0(r));          // m = 0 weights of tap r
-      const T wv1 = T(kWV0(4 - r)), wd1 = -T(kWD0(4 - r));  // m = 1 weights of tap r
+      const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
+      const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
 #pragma unroll
       for (int ff = 0; ff < 6; ++ff) {
         const T x = src[ff * 5 * SA_C + r];
@@ -308,14 +308,14 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += (kRowMirror ? T(kWV0(r)) : wvl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wv0<T>(r) : wvl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
     return v;
   };
   auto td = [&](int c, int k) {
     asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += (kRowMirror ? T(kWD0(r)) : wdl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wd0<T>(r) : wdl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
     return kRowMirror ? sgn * v : v;
   };
   const T dt = T(ctl->dt);
@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
       const T x = row0[r * rstep + c * SB_RC + k * SB_K];
-      v += (kRowMirror ? T(kWV0(r)) : wvl[r]) * x;
-      d += (kRowMirror ? T(kWD0(r)) : wdl[r]) * x;
+      v += (kRowMirror ? wv0<T>(r) : wvl[r]) * x;
+      d += (kRowMirror ? wd0<T>(r) : wdl[r]) * x;
     }
     if (kRowMirror) d *= sgn;
   };
