@@ -750,3 +750,63 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
   free(qn);
   return rc;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Volume diagnostics (readings O-24, O-25): on a ghosted block with ghosts filled.
+ *   E_k   = 1/(rho0 Omega) sum 1/2 rho |U|^2 dV
+ *   zeta  = 1/(rho0 Omega) sum 1/2 rho |omega|^2 dV, omega = curl U    (O-24)
+ *   eps_s = mu/(rho0 Omega) sum omega.omega dV                         (first term)
+ *   eps_d = 4/3 mu/(rho0 Omega) sum (div U)^2 dV                       (second term)
+ * plus the conservation monitors sum rho dV, sum rho U dV (3), sum rho E dV and Omega.
+ * Velocity derivatives at a cell centre (O-25): the fourth-order central difference in the cell
+ * index of the cell-average velocities, times the metric J = d(index)/dx at the cell centre:
+ *   du/dx_d (j) = J(j + 1/2) [8 (u_{j+1} - u_{j-1}) - (u_{j+2} - u_{j-2})] / 12.
+ * mu is mu_ref (the paper's eps_com takes a constant mu).
+ * ---------------------------------------------------------------------------------------- */
+static double vel_at(const or_grid* gr, const double* qg, int c, int i, int j, int k) {
+  return qg[gidx(gr, 1 + c, i, j, k)] / qg[gidx(gr, 0, i, j, k)];
+}
+
+void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double rho0, double out[OR_NDIAG]) {
+  double acc[OR_NDIAG] = {0};
+  for (int k = 0; k < gr->n[2]; ++k)
+    for (int j = 0; j < gr->n[1]; ++j)
+      for (int i = 0; i < gr->n[0]; ++i) {
+        int ijk[3] = {i, j, k};
+        double vol = cell_width(gr, 0, i) * cell_width(gr, 1, j) * cell_width(gr, 2, k);
+        double rho = qg[gidx(gr, 0, i, j, k)];
+        double u[3], grad[3][3]; /* grad[c][d] = d u_c / d x_d */
+        for (int c = 0; c < 3; ++c) u[c] = qg[gidx(gr, 1 + c, i, j, k)] / rho;
+        for (int d = 0; d < 3; ++d) {
+          double J = or_axis_metric(gr, d, ijk[d] + 0.5);
+          for (int c = 0; c < 3; ++c) {
+            int a[3], b[3], a2[3], b2[3];
+            for (int e = 0; e < 3; ++e) a[e] = b[e] = a2[e] = b2[e] = ijk[e];
+            a[d] += 1;
+            b[d] -= 1;
+            a2[d] += 2;
+            b2[d] -= 2;
+            double d1 = vel_at(gr, qg, c, a[0], a[1], a[2]) - vel_at(gr, qg, c, b[0], b[1], b[2]);
+            double d2 = vel_at(gr, qg, c, a2[0], a2[1], a2[2]) - vel_at(gr, qg, c, b2[0], b2[1], b2[2]);
+            grad[c][d] = J * (8.0 * d1 - d2) / 12.0;
+          }
+        }
+        double om[3] = {grad[2][1] - grad[1][2], grad[0][2] - grad[2][0], grad[1][0] - grad[0][1]};
+        double om2 = om[0] * om[0] + om[1] * om[1] + om[2] * om[2];
+        double dv = grad[0][0] + grad[1][1] + grad[2][2];
+        acc[OR_DIAG_EK] += 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * vol;
+        acc[OR_DIAG_ENSTROPHY] += 0.5 * rho * om2 * vol;
+        acc[OR_DIAG_EPS_S] += om2 * vol;
+        acc[OR_DIAG_EPS_D] += dv * dv * vol;
+        acc[OR_DIAG_MASS] += rho * vol;
+        for (int c = 0; c < 3; ++c) acc[OR_DIAG_MOM_X + c] += qg[gidx(gr, 1 + c, i, j, k)] * vol;
+        acc[OR_DIAG_ENERGY] += qg[gidx(gr, 4, i, j, k)] * vol;
+        acc[OR_DIAG_VOLUME] += vol;
+      }
+  double omega = acc[OR_DIAG_VOLUME];
+  for (int v = 0; v < OR_NDIAG; ++v) out[v] = acc[v];
+  out[OR_DIAG_EK] = acc[OR_DIAG_EK] / (rho0 * omega);
+  out[OR_DIAG_ENSTROPHY] = acc[OR_DIAG_ENSTROPHY] / (rho0 * omega);
+  out[OR_DIAG_EPS_S] = g->mu_ref * acc[OR_DIAG_EPS_S] / (rho0 * omega);
+  out[OR_DIAG_EPS_D] = 4.0 / 3.0 * g->mu_ref * acc[OR_DIAG_EPS_D] / (rho0 * omega);
+}

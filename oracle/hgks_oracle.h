@@ -137,6 +137,17 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
            double cfl, double* dt_hist);
 
 /* Number of OpenMP threads the oracle uses (1 when built without OpenMP). */
+/* Volume diagnostics of a ghosted block (ghosts filled): E_k, enstrophy (O-24),
+ * the two terms of eps_com (mu = mu_ref), and conservation monitors; velocity
+ * derivatives by O-25 (fourth-order central in the cell index times J at the cell centre).
+ * Pins (test_oracle_diagnostics.py): TGV closed forms E_k = 1/8, zeta = 3/8 kappa(h)^2 with
+ * kappa(h) = (8 sin h - sin 2h)/(6h) the exact symbol of the difference, div U = 0; a potential
+ * flow (omega = 0, eps_d closed form); a linear shear on a tanh-stretched axis (metric); Omega. */
+#define OR_NDIAG 10
+enum { OR_DIAG_EK = 0, OR_DIAG_ENSTROPHY, OR_DIAG_EPS_S, OR_DIAG_EPS_D, OR_DIAG_MASS, OR_DIAG_MOM_X,
+       OR_DIAG_MOM_Y, OR_DIAG_MOM_Z, OR_DIAG_ENERGY, OR_DIAG_VOLUME };
+void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double rho0, double out[OR_NDIAG]);
+
 int or_num_threads(void);
 
 #ifdef __cplusplus

@@ -78,6 +78,7 @@ def lib():
         L.or_cfl_dt.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double]
         L.or_run.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_int, C.c_double,
                              C.c_double, _dp]
+        L.or_diagnostics.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double, _dp]
         L.or_num_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -250,6 +251,25 @@ def run(gas: Gas, q: np.ndarray, dx, nsteps: int, dt_fixed: float = 0.0, cfl: fl
     if rc:
         raise ValueError("oracle run hit an invalid state")
     return q, hist[:nsteps]
+
+
+DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
+
+
+def diagnostics(gas: Gas, q: np.ndarray | None = None, dx=None, rho0: float = 1.0, qg: np.ndarray | None = None,
+                grid: Grid | None = None) -> np.ndarray:
+    """Volume diagnostics (or_diagnostics) of a state (ghosts filled by the oracle) or of a
+    pre-ghosted block qg (ghosts as given).  Returns the OR_NDIAG vector in DIAG_NAMES order."""
+    if qg is None:
+        q = _arr(q)
+        gr = _grid_of(q, dx, grid)
+        qg = ghosted(q, gas=gas, grid=gr)
+    else:
+        qg = _arr(qg)
+        gr = grid if grid is not None else make_grid(tuple(s - 6 for s in qg.shape[:0:-1]), dx)
+    out = np.zeros(len(DIAG_NAMES))
+    lib().or_diagnostics(C.byref(gas), C.byref(gr), _p(qg), rho0, _p(out))
+    return out
 
 
 def num_threads() -> int:
