@@ -108,6 +108,29 @@ int hgks_destroy(hgks_ctx* c);
 /* Last error message of c (or of the calling thread when c == NULL); never NULL. */
 const char* hgks_last_error(const hgks_ctx* c);
 
+/* ---- diagnostics ---------------------------------------------------- */
+
+/* Volume integrals of the current state over the WHOLE domain (collective: every rank calls it,
+ * every rank receives the global values).  P:889-903 define E_k and eps_com; O-24/O-25:
+ *   out[HGKS_DIAG_EK]        E_k   = 1/(rho0 Omega) sum 1/2 rho |U|^2 dV
+ *   out[HGKS_DIAG_ENSTROPHY] zeta  = 1/(rho0 Omega) sum 1/2 rho |omega|^2 dV, omega = curl U
+ *   out[HGKS_DIAG_EPS_S]     mu/(rho0 Omega) sum |omega|^2 dV          (eps_com, first term)
+ *   out[HGKS_DIAG_EPS_D]     4/3 mu/(rho0 Omega) sum (div U)^2 dV      (eps_com, second term)
+ *   out[HGKS_DIAG_MASS..ENERGY]  sum rho dV, sum rho U dV (x, y, z), sum rho E dV
+ *   out[HGKS_DIAG_VOLUME]    Omega = sum dV
+ * mu = params.mu_ref.  Velocity derivatives: fourth-order central difference in the cell index
+ * times d(index)/dx at the cell centre, ghosts as the step fills them (periodic, wall mirror,
+ * halo).  Computed in fp64 for either precision by a fixed-order (deterministic) two-pass
+ * reduction, then an NCCL sum over ranks.  rho0 > 0.  Synchronises the stream.
+ * Errors: HGKS_EINVAL (NULL, no state, rho0 <= 0), HGKS_ECUDA, HGKS_ENCCL. */
+#define HGKS_DIAG_COUNT 10
+typedef enum {
+  HGKS_DIAG_EK = 0, HGKS_DIAG_ENSTROPHY = 1, HGKS_DIAG_EPS_S = 2, HGKS_DIAG_EPS_D = 3,
+  HGKS_DIAG_MASS = 4, HGKS_DIAG_MOM_X = 5, HGKS_DIAG_MOM_Y = 6, HGKS_DIAG_MOM_Z = 7,
+  HGKS_DIAG_ENERGY = 8, HGKS_DIAG_VOLUME = 9
+} hgks_diag;
+int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]);
+
 /* ---- small helpers (host logic, no device work) ----------------------------------------- */
 
 /* Size of the opaque NCCL unique id (128) and generator for rank 0 (broadcast it yourself). */

@@ -712,8 +712,48 @@ static void to_ghosted(const or_grid* gr, const double* q, double* qg) {
         for (int i = 0; i < gr->n[0]; ++i) qg[gidx(gr, v, i, j, k)] = q[cidx(gr, v, i, j, k)];
 }
 
-int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed, double cfl,
-           double* dt_hist) {
+/* ------------------------------------------------------------------------------------------
+ * Streamwise body force (channel; "the constant moment flux in the streamwise
+ * direction is used to determine the external force").  The paper does not give the discrete
+ * form; readings O-26 / O-27:
+ *  O-26 a uniform acceleration f along x, constant over a step, enters as the source
+ *       S(Q) = (0, rho f, 0, 0, rho U f) of L, and its time derivative through dS/dt = S'(Q) dQ/dt
+ *       = (0, f L_rho, 0, 0, f L_rhoU) with L the source-inclusive operator.  Stage 2 evaluates no
+ *       flux (only d_t L(Q*)), so L(Q*) in S'(Q*) L(Q*) is its Taylor value L(Q^n) + dt/2 d_t L(Q^n).
+ *  O-27 mode 2 chooses f each step so that the bulk momentum m = (1/Omega) sum rho U dV returns to
+ *       the target m_b in one step if the wall drag stays as in the previous step (dead-beat):
+ *         f^n = f^{n-1} + [ (m_b - m^n)/dt^n - (m^n - m^{n-1})/dt^{n-1} ] / rho_b^n,
+ *       rho_b = (1/Omega) sum rho dV, with f^{-1} = f_init and m^{-1} = m^0 (first step:
+ *       f^0 = f_init + (m_b - m^0)/(dt^0 rho_b^0)).  Mode 1: f = f_init every step.
+ * ---------------------------------------------------------------------------------------- */
+static void bulk_of(const or_grid* gr, const double* q, double* m, double* rho_b) {
+  long ncell = (long)gr->n[0] * gr->n[1] * gr->n[2];
+  double sm = 0.0, sr = 0.0, vol = 0.0;
+  for (int k = 0; k < gr->n[2]; ++k)
+    for (int j = 0; j < gr->n[1]; ++j)
+      for (int i = 0; i < gr->n[0]; ++i) {
+        double dv = cell_width(gr, 0, i) * cell_width(gr, 1, j) * cell_width(gr, 2, k);
+        sr += q[cidx(gr, 0, i, j, k)] * dv;
+        sm += q[cidx(gr, 1, i, j, k)] * dv;
+        vol += dv;
+      }
+  (void)ncell;
+  *m = sm / vol;
+  *rho_b = sr / vol;
+}
+
+/* O-26: add the source and its time derivative to (L, dL) of state q (all [5][ncell]) */
+static void add_force(long ncell, const double* q, double f, double* L, double* dL) {
+  for (long s = 0; s < ncell; ++s) {
+    L[1 * ncell + s] += q[0 * ncell + s] * f;
+    L[4 * ncell + s] += q[1 * ncell + s] * f;
+    dL[1 * ncell + s] += f * L[0 * ncell + s];
+    dL[4 * ncell + s] += f * L[1 * ncell + s];
+  }
+}
+
+int or_run_forced(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed, double cfl,
+                  const or_forcing* fc, double* dt_hist, double* f_hist) {
   long ncell = (long)gr->n[0] * gr->n[1] * gr->n[2];
   long ng = 5L * (gr->n[0] + 2 * OR_NG) * (gr->n[1] + 2 * OR_NG) * (gr->n[2] + 2 * OR_NG);
   double* qg = (double*)calloc(ng, sizeof(double));
@@ -723,20 +763,41 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
   double* dLs = (double*)malloc(sizeof(double) * 5 * ncell);
   double* qs = (double*)malloc(sizeof(double) * 5 * ncell);
   double* qn = (double*)malloc(sizeof(double) * 5 * ncell);
+  int mode = fc ? fc->mode : 0;
+  double f_prev = fc ? fc->force : 0.0, m_prev = 0.0, dt_prev = 0.0;
   int rc = 0;
   if (!state_valid(g, ncell, q)) rc = -1;
   for (int step = 0; step < nsteps && rc == 0; ++step) {
     double dt = dt_fixed > 0.0 ? dt_fixed : or_cfl_dt(g, gr, q, cfl);
     if (dt_hist) dt_hist[step] = dt;
+    double f = 0.0;
+    if (mode == 1) {
+      f = fc->force;
+    } else if (mode == 2) { /* O-27 */
+      double m, rb;
+      bulk_of(gr, q, &m, &rb);
+      if (step == 0) f = f_prev + (fc->target - m) / (dt * rb);
+      else f = f_prev + ((fc->target - m) / dt - (m - m_prev) / dt_prev) / rb;
+      m_prev = m;
+      dt_prev = dt;
+      f_prev = f;
+    }
+    if (f_hist) f_hist[step] = f;
     /* stage 1 at Q^n */
     to_ghosted(gr, q, qg);
     or_fill_ghosts(g, gr, qg);
     if (or_operator(g, gr, qg, dt, L, dL)) { rc = -1; break; }
+    if (mode) add_force(ncell, q, f, L, dL);
     or_s2o4_stage1(5 * ncell, q, L, dL, dt, qs);
     /* stage 2 at Q* (same dt and windows, O-11) */
     to_ghosted(gr, qs, qg);
     or_fill_ghosts(g, gr, qg);
     if (or_operator(g, gr, qg, dt, Ls, dLs)) { rc = -1; break; }
+    if (mode) /* O-26: S'(Q*) L(Q*), L(Q*) ~ L(Q^n) + dt/2 d_t L(Q^n) */
+      for (long s = 0; s < ncell; ++s) {
+        dLs[1 * ncell + s] += f * (L[0 * ncell + s] + 0.5 * dt * dL[0 * ncell + s]);
+        dLs[4 * ncell + s] += f * (L[1 * ncell + s] + 0.5 * dt * dL[1 * ncell + s]);
+      }
     or_s2o4_final(5 * ncell, q, L, dL, dLs, dt, qn);
     if (!state_valid(g, ncell, qn)) { rc = -1; break; }
     memcpy(q, qn, sizeof(double) * 5 * ncell);
@@ -749,6 +810,11 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
   free(qs);
   free(qn);
   return rc;
+}
+
+int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed, double cfl,
+           double* dt_hist) {
+  return or_run_forced(g, gr, q, nsteps, dt_fixed, cfl, NULL, dt_hist, NULL);
 }
 
 /* ------------------------------------------------------------------------------------------

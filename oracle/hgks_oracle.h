@@ -136,6 +136,21 @@ double or_cfl_dt(const or_gas* g, const or_grid* gr, const double* q, double cfl
 int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed,
            double cfl, double* dt_hist);
 
+/* Streamwise body force (readings O-26 source, O-27 dead-beat bulk-momentum
+ * controller, both restated at or_run_forced in hgks_oracle.c and in DESIGN.md).
+ * mode 0 none, 1 constant acceleration f = force, 2 constant bulk momentum target (f_init = force).
+ * f_hist[step] = f applied in that step.  Pins (test_oracle_forcing.py): uniform flow under a
+ * constant acceleration is integrated exactly (U = U0 + f t, p unchanged); the dead-beat step
+ * reaches the target in one step in a drag-free box with the closed-form f; laminar Poiseuille
+ * balance f rho_b = tau_w / H (f = 3 mu U_b / (rho_b H^2)). */
+typedef struct {
+  int mode;
+  double force;   /* mode 1: f ; mode 2: f_init */
+  double target;  /* mode 2: bulk momentum m_b = (1/Omega) sum rho U dV */
+} or_forcing;
+int or_run_forced(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed, double cfl,
+                  const or_forcing* fc, double* dt_hist, double* f_hist);
+
 /* Number of OpenMP threads the oracle uses (1 when built without OpenMP). */
 /* Volume diagnostics of a ghosted block (ghosts filled): E_k, enstrophy (O-24),
  * the two terms of eps_com (mu = mu_ref), and conservation monitors; velocity

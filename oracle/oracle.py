@@ -45,6 +45,10 @@ class Grid(C.Structure):
                 ("stretch_b", C.c_double * 3)]
 
 
+class Forcing(C.Structure):
+    _fields_ = [("mode", C.c_int), ("force", C.c_double), ("target", C.c_double)]
+
+
 _lib = None
 
 
@@ -78,6 +82,8 @@ def lib():
         L.or_cfl_dt.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double]
         L.or_run.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_int, C.c_double,
                              C.c_double, _dp]
+        L.or_run_forced.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_int, C.c_double, C.c_double,
+                                    C.POINTER(Forcing), _dp, _dp]
         L.or_diagnostics.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double, _dp]
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -270,6 +276,20 @@ def diagnostics(gas: Gas, q: np.ndarray | None = None, dx=None, rho0: float = 1.
     out = np.zeros(len(DIAG_NAMES))
     lib().or_diagnostics(C.byref(gas), C.byref(gr), _p(qg), rho0, _p(out))
     return out
+
+
+def run_forced(gas: Gas, q: np.ndarray, dx, nsteps: int, mode: int, force: float = 0.0, target: float = 0.0,
+               dt_fixed: float = 0.0, cfl: float = 0.4, grid: Grid | None = None):
+    """or_run_forced: returns (q_new, dt_history, force_history)."""
+    q = _arr(q).copy()
+    hist = np.zeros(max(nsteps, 1))
+    fh = np.zeros(max(nsteps, 1))
+    fc = Forcing(mode, force, target)
+    rc = lib().or_run_forced(C.byref(gas), C.byref(_grid_of(q, dx, grid)), _p(q), nsteps, dt_fixed, cfl,
+                             C.byref(fc), _p(hist), _p(fh))
+    if rc:
+        raise ValueError("oracle run hit an invalid state")
+    return q, hist[:nsteps], fh[:nsteps]
 
 
 def num_threads() -> int:

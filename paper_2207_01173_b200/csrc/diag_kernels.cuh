@@ -1,0 +1,119 @@
+// diag_kernels.cuh — on-device volume diagnostics (O-24, O-25).
+//
+//   diag_kernel<T>      per-cell terms of E_k, enstrophy, |omega|^2, (div U)^2 and the conservation
+//                       monitors, summed per block in a fixed order (fp64 for either precision)
+//   diag_final_kernel   one block: fixed-order sum of the block partials -> NDIAG doubles
+//
+// Deterministic: a fixed grid (DIAG_BLOCKS x DIAG_TPB), a fixed grid-stride cell order per thread
+// and fixed tree reductions, so repeated calls on the same state return identical bits.
+#pragma once
+#include "hgks_kernels.cuh"
+
+namespace hgks {
+
+constexpr int NDIAG = 10;  // HGKS_DIAG_COUNT
+constexpr int DIAG_TPB = 256;
+constexpr int DIAG_BLOCKS = 148 * 4;
+
+// fp64 cell-centre metric J = d(index)/dx and cell widths of every axis (local cell index)
+struct DiagGeo {
+  const double* jc[3];
+  const double* w[3];
+};
+
+template <typename T>
+__device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& g, int c, int i, int j, int k) {
+  return (double)q[qidx(g, 1 + c, i, j, k)] / (double)q[qidx(g, 0, i, j, k)];
+}
+
+// sum v[0..N) over the block (fixed tree order); result valid in thread 0
+template <int N>
+__device__ __forceinline__ void block_sum_fixed(double (&v)[N], double* sh) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] = v[n];
+  __syncthreads();
+  for (int s = DIAG_TPB / 2; s > 0; s >>= 1) {
+    if (t < s) {
+#pragma unroll
+      for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] += sh[n * DIAG_TPB + t + s];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) v[n] = sh[n * DIAG_TPB];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q, Geo<T> g, DiagGeo dg,
+                                                        double* __restrict__ partial) {
+  __shared__ double sh[NDIAG * DIAG_TPB];
+  double acc[NDIAG];
+#pragma unroll
+  for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
+  const int nx = g.n[0], ny = g.n[1];
+  const long long ncell = (long long)nx * ny * g.n[2];
+  for (long long e = blockIdx.x * (long long)DIAG_TPB + threadIdx.x; e < ncell; e += (long long)gridDim.x * DIAG_TPB) {
+    const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
+    const int ijk[3] = {i, j, k};
+    const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
+    const double rho = (double)q[qidx(g, 0, i, j, k)];
+    double u[3], m[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      m[c] = (double)q[qidx(g, 1 + c, i, j, k)];
+      u[c] = m[c] / rho;
+    }
+    double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double J = dg.jc[d][ijk[d]];
+      const int di = d == 0, dj = d == 1, dk = d == 2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double d1 = vel_of(q, g, c, i + di, j + dj, k + dk) - vel_of(q, g, c, i - di, j - dj, k - dk);
+        const double d2 = vel_of(q, g, c, i + 2 * di, j + 2 * dj, k + 2 * dk) -
+                          vel_of(q, g, c, i - 2 * di, j - 2 * dj, k - 2 * dk);
+        grad[c][d] = J * (8.0 * d1 - d2) / 12.0;
+      }
+    }
+    const double o0 = grad[2][1] - grad[1][2], o1 = grad[0][2] - grad[2][0], o2 = grad[1][0] - grad[0][1];
+    const double om2 = o0 * o0 + o1 * o1 + o2 * o2;
+    const double dv = grad[0][0] + grad[1][1] + grad[2][2];
+    acc[0] += 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * vol;
+    acc[1] += 0.5 * rho * om2 * vol;
+    acc[2] += om2 * vol;
+    acc[3] += dv * dv * vol;
+    acc[4] += rho * vol;
+    acc[5] += m[0] * vol;
+    acc[6] += m[1] * vol;
+    acc[7] += m[2] * vol;
+    acc[8] += (double)q[qidx(g, 4, i, j, k)] * vol;
+    acc[9] += vol;
+  }
+  block_sum_fixed(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < NDIAG; ++n) partial[blockIdx.x * NDIAG + n] = acc[n];
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(DIAG_TPB) diag_final_kernel(const double* __restrict__ partial, int nblocks,
+                                                              double* __restrict__ out) {
+  __shared__ double sh[N * DIAG_TPB];
+  double acc[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) acc[n] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += DIAG_TPB) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) acc[n] += partial[b * N + n];
+  }
+  block_sum_fixed(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) out[n] = acc[n];
+  }
+}
+
+}  // namespace hgks

@@ -17,6 +17,7 @@
 #include "../../include/hgks.h"
 #include "../../include/hgks_test.h"
 #include "hgks_kernels.cuh"
+#include "diag_kernels.cuh"
 
 using namespace hgks;
 
@@ -62,6 +63,9 @@ struct hgks_ctx {
   void* F[3] = {nullptr, nullptr, nullptr};
   void* metric = nullptr;   // per axis: jf[n+1], jg[2n], iw[n] (T), see Geo
   size_t metric_off[3][3] = {};
+  double* dmetric = nullptr;  // fp64 per axis: J at the cell centres [n], cell widths [n] (diagnostics)
+  double* diag_dev = nullptr; // DIAG_BLOCKS * NDIAG block partials, then NDIAG results
+  double* diag_host = nullptr;  // pinned NDIAG
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
   cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
@@ -156,13 +160,15 @@ static Geo<T> make_geo(const hgks_ctx* c) {
 // Metric tables of one axis (reading O-18), computed here in fp64: the reconstruction works in the
 // uniform cell-index coordinate zeta (face j at zeta = j); J = d zeta / dx.  For HGKS_TANH,
 // x(zeta) = (lo+hi)/2 + (hi-lo)/2 tanh(b (2 zeta/N - 1)) / tanh(b).
-static void axis_tables(const hgks_params& p, int d, int N, int j0, int n, double* jf, double* jg, double* iw) {
+static void axis_tables(const hgks_params& p, int d, int N, int j0, int n, double* jf, double* jg, double* iw,
+                        double* jc, double* wc) {
   const double lo = p.lo[d], hi = p.hi[d];
   if (p.stretch[d] != HGKS_TANH) {
-    const double ih = N / (hi - lo);
+    const double ih = N / (hi - lo), h = (hi - lo) / N;
     for (int j = 0; j <= n; ++j) jf[j] = ih;
     for (int j = 0; j < 2 * n; ++j) jg[j] = ih;
-    for (int j = 0; j < n; ++j) iw[j] = ih;
+    for (int j = 0; j < n; ++j) iw[j] = jc[j] = ih;
+    for (int j = 0; j < n; ++j) wc[j] = h;
     return;
   }
   const double b = p.stretch_b[d], tb = tanh(b), hh = 0.5 * (hi - lo), cc = 0.5 * (lo + hi);
@@ -177,6 +183,8 @@ static void axis_tables(const hgks_params& p, int d, int N, int j0, int n, doubl
     jg[j] = J(j0 + j + 0.5 - s3);
     jg[n + j] = J(j0 + j + 0.5 + s3);
     iw[j] = 1.0 / (x(j0 + j + 1) - x(j0 + j));
+    jc[j] = J(j0 + j + 0.5);
+    wc[j] = x(j0 + j + 1) - x(j0 + j);
   }
 }
 
@@ -466,8 +474,16 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
       tot += (nloc[d] + 1) + 2 * nloc[d] + nloc[d];
     }
     double* h = (double*)malloc(tot * sizeof(double));
-    for (int d = 0; d < 3; ++d)
-      axis_tables(*p, d, p->n[d], j0[d], nloc[d], h + c->metric_off[d][0], h + c->metric_off[d][1], h + c->metric_off[d][2]);
+    const size_t dtot = 2 * ((size_t)nloc[0] + nloc[1] + nloc[2]);
+    double* hd = (double*)malloc(dtot * sizeof(double));
+    for (int d = 0, off = 0; d < 3; off += 2 * nloc[d], ++d)
+      axis_tables(*p, d, p->n[d], j0[d], nloc[d], h + c->metric_off[d][0], h + c->metric_off[d][1], h + c->metric_off[d][2],
+                  hd + off, hd + off + nloc[d]);
+    ok = ok && cudaMalloc(&c->dmetric, dtot * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMemcpy(c->dmetric, hd, dtot * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+    free(hd);
+    ok = ok && cudaMalloc(&c->diag_dev, (DIAG_BLOCKS + 1) * NDIAG * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&c->diag_host, NDIAG * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->metric, tot * c->esz) == cudaSuccess;
     if (ok) {
       if (c->fp32) {
@@ -626,6 +642,55 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   return HGKS_OK;
 }
 
+}  // extern "C"
+
+template <typename T>
+static int diagnostics_t(hgks_ctx* c) {
+  Geo<T> g = make_geo<T>(c);
+  T* Q = (T*)c->Q[c->cur];
+  // ghosts of the current state (a halted hgks_step leaves ctl->halt set, which gates the ghost
+  // kernels; hgks_step resets it on entry anyway)
+  CUDA_TRY(c, cudaMemsetAsync(&c->ctl->halt, 0, sizeof(int), c->s));
+  int rc;
+  if ((rc = fill_ghosts<T>(c, Q))) return rc;
+  DiagGeo dg;
+  const int nloc[3] = {c->n[0], c->n[1], c->nzl};
+  for (int d = 0, off = 0; d < 3; off += 2 * nloc[d], ++d) {
+    dg.jc[d] = c->dmetric + off;
+    dg.w[d] = c->dmetric + off + nloc[d];
+  }
+  double* out = c->diag_dev + DIAG_BLOCKS * NDIAG;
+  diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->diag_dev);
+  diag_final_kernel<NDIAG><<<1, DIAG_TPB, 0, c->s>>>(c->diag_dev, DIAG_BLOCKS, out);
+  c->total_launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(out, out, NDIAG, ncclFloat64, ncclSum, c->comm, c->s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->diag_host, out, NDIAG * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  return HGKS_OK;
+}
+
+extern "C" {
+
+int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_diagnostics: ctx is NULL");
+  if (!out) return fail(c, HGKS_EINVAL, "hgks_diagnostics: out is NULL");
+  if (!(rho0 > 0.0)) return fail(c, HGKS_EINVAL, "hgks_diagnostics: rho0 must be > 0");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_diagnostics: no state set");
+  static_assert(HGKS_DIAG_COUNT == NDIAG, "diagnostic count");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  int rc = c->fp32 ? diagnostics_t<float>(c) : diagnostics_t<double>(c);
+  if (rc) return rc;
+  const double* a = c->diag_host;
+  const double vol = a[HGKS_DIAG_VOLUME], mu = c->p.mu_ref;
+  for (int k = 0; k < NDIAG; ++k) out[k] = a[k];
+  out[HGKS_DIAG_EK] = a[HGKS_DIAG_EK] / (rho0 * vol);
+  out[HGKS_DIAG_ENSTROPHY] = a[HGKS_DIAG_ENSTROPHY] / (rho0 * vol);
+  out[HGKS_DIAG_EPS_S] = mu * a[HGKS_DIAG_EPS_S] / (rho0 * vol);
+  out[HGKS_DIAG_EPS_D] = 4.0 / 3.0 * mu * a[HGKS_DIAG_EPS_D] / (rho0 * vol);
+  return HGKS_OK;
+}
+
 int hgks_destroy(hgks_ctx* c) {
   if (!c) return HGKS_OK;
   cudaSetDevice(c->dev);
@@ -636,6 +701,9 @@ int hgks_destroy(hgks_ctx* c) {
   for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
   for (int b = 0; b < 2; ++b) cudaFree(c->FF[b]);
   cudaFree(c->metric);
+  cudaFree(c->dmetric);
+  cudaFree(c->diag_dev);
+  if (c->diag_host) cudaFreeHost(c->diag_host);
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   for (int d = 0; d < 3; ++d) {

@@ -28,7 +28,8 @@ KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt",
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+            "hgks_diagnostics", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
 
 
 class HgksError(RuntimeError):
@@ -77,6 +78,7 @@ def lib():
         L.hgks_get_nccl_id.argtypes = [vp]
         L.hgks_slab_of.argtypes = [C.c_int32] * 3 + [C.POINTER(C.c_int32)] * 2
         L.hgks_make_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(HaloPlan)]
+        L.hgks_diagnostics.argtypes = [vp, C.c_double, _dp]
         L.hgks_profile_enable.argtypes = [vp, C.c_int]
         L.hgks_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.hgks_test_gp_flux.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
@@ -183,6 +185,13 @@ def hgks_step(ctx, nsteps: int, t: float = 0.0, t_end: float = 0.0):
     return tt.value, dtl.value
 
 
+def hgks_diagnostics(ctx, rho0: float = 1.0) -> np.ndarray:
+    """Global volume diagnostics of the current state (collective), in DIAG_NAMES order."""
+    out = np.zeros(len(DIAG_NAMES))
+    _check(lib().hgks_diagnostics(ctx, rho0, out.ctypes.data_as(_dp)), ctx)
+    return out
+
+
 def hgks_profile_enable(ctx, enable: bool = True) -> None:
     _check(lib().hgks_profile_enable(ctx, int(enable)), ctx)
 
@@ -242,6 +251,9 @@ class Solver:
     def step(self, nsteps: int = 1, t_end: float = 0.0):
         self.t, dt = hgks_step(self.ctx, nsteps, self.t, t_end)
         return dt
+
+    def diagnostics(self, rho0: float = 1.0) -> dict:
+        return dict(zip(DIAG_NAMES, hgks_diagnostics(self.ctx, rho0)))
 
     def get_state(self, out=None):
         if out is None:
