@@ -49,6 +49,16 @@ typedef enum { HGKS_FP64 = 0, HGKS_FP32 = 1 } hgks_precision;      /* P:1091-109
 typedef enum { HGKS_PERIODIC = 0, HGKS_WALL_ISOTHERMAL = 1 } hgks_bc; /* P:500-504, P:962-964        */
 typedef enum { HGKS_UNIFORM = 0, HGKS_TANH = 1 } hgks_stretch;       /* P:945-956 channel mesh        */
 typedef enum { HGKS_MU_CONST = 0, HGKS_MU_POWER = 1 } hgks_mu_law;   /* P:971-972                    */
+/* streamwise (x) body force, P:964-965 "the constant moment flux in the streamwise direction is
+ * used to determine the external force"; discrete form = readings O-26 / O-27 (DESIGN.md):
+ *   O-26 a uniform acceleration f, constant over a step, is the source S = (0, rho f, 0, 0, rho U f)
+ *        of L, with d_t S = (0, f L_rho, 0, 0, f L_rhoU); in stage 2, L(Q*) in that product is its
+ *        Taylor value L(Q^n) + dt/2 d_t L(Q^n) (stage 2 evaluates no flux);
+ *   O-27 HGKS_FORCE_BULK chooses f every step (dead-beat on the bulk momentum
+ *        m = (1/Omega) sum rho U dV, rho_b = (1/Omega) sum rho dV, target m_b):
+ *          f^n = f^{n-1} + [ (m_b - m^n)/dt^n - (m^n - m^{n-1})/dt^{n-1} ] / rho_b^n,
+ *        first step after set_state: f^0 = force + (m_b - m^0)/(dt^0 rho_b^0).                     */
+typedef enum { HGKS_FORCE_NONE = 0, HGKS_FORCE_CONST = 1, HGKS_FORCE_BULK = 2 } hgks_force_mode;
 
 typedef struct {
   int32_t n[3];          /* GLOBAL interior cells (nx, ny, nz); each >= 5; nz/nranks >= 3           */
@@ -74,6 +84,9 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal used by this context                              */
   const void* nccl_id;   /* 128-byte ncclUniqueId identical on all ranks; NULL iff nranks == 1     */
   void* stream;          /* cudaStream_t for all work; NULL => the library creates one            */
+  hgks_force_mode force_mode; /* streamwise body force (see hgks_force_mode); NONE for TGV           */
+  double force;          /* CONST: the acceleration f; BULK: f before the first step (f_init)      */
+  double force_target;   /* BULK: target bulk momentum m_b (e.g. rho_b U_b = 1 for the channel)    */
 } hgks_params;
 
 /* Validate p, allocate device memory, create streams and (nranks > 1) the NCCL communicator.
@@ -130,6 +143,11 @@ typedef enum {
   HGKS_DIAG_ENERGY = 8, HGKS_DIAG_VOLUME = 9
 } hgks_diag;
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]);
+
+/* Streamwise force state (collective, synchronises): *force = f applied in the last committed step
+ * (the params' force before the first step); *bulk_momentum, *bulk_density = m and rho_b of the
+ * current state (HGKS_FORCE_BULK; 0 otherwise).  Any output pointer may be NULL. */
+int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* bulk_density);
 
 /* ---- small helpers (host logic, no device work) ----------------------------------------- */
 

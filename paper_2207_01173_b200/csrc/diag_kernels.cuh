@@ -12,36 +12,11 @@
 namespace hgks {
 
 constexpr int NDIAG = 10;  // HGKS_DIAG_COUNT
-constexpr int DIAG_TPB = 256;
 constexpr int DIAG_BLOCKS = 148 * 4;
-
-// fp64 cell-centre metric J = d(index)/dx and cell widths of every axis (local cell index)
-struct DiagGeo {
-  const double* jc[3];
-  const double* w[3];
-};
 
 template <typename T>
 __device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& g, int c, int i, int j, int k) {
   return (double)q[qidx(g, 1 + c, i, j, k)] / (double)q[qidx(g, 0, i, j, k)];
-}
-
-// sum v[0..N) over the block (fixed tree order); result valid in thread 0
-template <int N>
-__device__ __forceinline__ void block_sum_fixed(double (&v)[N], double* sh) {
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] = v[n];
-  __syncthreads();
-  for (int s = DIAG_TPB / 2; s > 0; s >>= 1) {
-    if (t < s) {
-#pragma unroll
-      for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] += sh[n * DIAG_TPB + t + s];
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int n = 0; n < N; ++n) v[n] = sh[n * DIAG_TPB];
 }
 
 template <typename T>

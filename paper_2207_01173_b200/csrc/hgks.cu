@@ -66,6 +66,7 @@ struct hgks_ctx {
   double* dmetric = nullptr;  // fp64 per axis: J at the cell centres [n], cell widths [n] (diagnostics)
   double* diag_dev = nullptr; // DIAG_BLOCKS * NDIAG block partials, then NDIAG results
   double* diag_host = nullptr;  // pinned NDIAG
+  double* bulk_dev = nullptr;   // 2 per update block: (sum rho dV, sum rho U dV) partials (O-27)
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
   cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
@@ -301,12 +302,45 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   return HGKS_OK;
 }
 
+static DiagGeo diag_geo(const hgks_ctx* c) {
+  DiagGeo dg;
+  const int nloc[3] = {c->n[0], c->n[1], c->nzl};
+  for (int d = 0, off = 0; d < 3; off += 2 * nloc[d], ++d) {
+    dg.jc[d] = c->dmetric + off;
+    dg.w[d] = c->dmetric + off + nloc[d];
+  }
+  return dg;
+}
+
+template <typename T>
+static int diagnostics_t(hgks_ctx* c) {
+  Geo<T> g = make_geo<T>(c);
+  T* Q = (T*)c->Q[c->cur];
+  // ghosts of the current state (a halted hgks_step leaves ctl->halt set, which gates the ghost
+  // kernels; hgks_step resets it on entry anyway)
+  CUDA_TRY(c, cudaMemsetAsync(&c->ctl->halt, 0, sizeof(int), c->s));
+  int rc;
+  if ((rc = fill_ghosts<T>(c, Q))) return rc;
+  const DiagGeo dg = diag_geo(c);
+  double* out = c->diag_dev + DIAG_BLOCKS * NDIAG;
+  diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->diag_dev);
+  diag_final_kernel<NDIAG><<<1, DIAG_TPB, 0, c->s>>>(c->diag_dev, DIAG_BLOCKS, out);
+  c->total_launches += 2;
+  CUDA_TRY(c, cudaGetLastError());
+  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(out, out, NDIAG, ncclFloat64, ncclSum, c->comm, c->s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->diag_host, out, NDIAG * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  return HGKS_OK;
+}
+
 template <typename T>
 static int run_steps(hgks_ctx* c, int nsteps) {
   Geo<T> g = make_geo<T>(c);
   const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   const int tpb = 256;
   const int ublocks = (int)((ncell + tpb - 1) / tpb);
+  const DiagGeo dg = diag_geo(c);
+  const bool bulk = c->p.force_mode == HGKS_FORCE_BULK;
   int rc;
   for (int s = 0; s < nsteps; ++s) {
     T* Qn = (T*)c->Q[c->cur];
@@ -320,18 +354,25 @@ static int run_steps(hgks_ctx* c, int nsteps) {
     if ((rc = fill_ghosts<T>(c, Qn))) return rc;
     if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
-    update_kernel<T, 1><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, c->p.gamma, c->ctl);
+    update_kernel<T, 1><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
+                                                   c->ctl, c->bulk_dev);
     prof_end(c, HGKS_K_UPDATE);
     // stage 2 at Q* (same dt and windows, O-11)
     if ((rc = fill_ghosts<T>(c, Qs))) return rc;
     if ((rc = flux_sweeps<T, 2>(c, Qs))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
-    update_kernel<T, 2><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, c->p.gamma, c->ctl);
+    update_kernel<T, 2><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
+                                                   c->ctl, c->bulk_dev);
     prof_end(c, HGKS_K_UPDATE);
     c->total_launches += 2;
+    if (bulk) {  // bulk momentum / density of Q^{n+1} for the force controller (O-27)
+      diag_final_kernel<2><<<1, DIAG_TPB, 0, c->s>>>(c->bulk_dev, ublocks, &c->ctl->bulk_new[0]);
+      c->total_launches += 1;
+    }
     CUDA_TRY(c, cudaGetLastError());
     if (c->p.nranks > 1) {  // global max wave speed + global error flag
       NCCL_TRY(c, ncclAllReduce(&c->ctl->red[0], &c->ctl->red[0], 2, ncclUint64, ncclMax, c->comm, c->s));
+      if (bulk) NCCL_TRY(c, ncclAllReduce(&c->ctl->bulk_new[0], &c->ctl->bulk_new[0], 2, ncclFloat64, ncclSum, c->comm, c->s));
     }
     c->cur ^= 1;
   }
@@ -402,6 +443,9 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   if (!(p->dt_fixed > 0.0) && !(p->cfl > 0.0)) return fail(nullptr, HGKS_EINVAL, "need cfl > 0 or dt_fixed > 0");
   if (p->precision != HGKS_FP64 && p->precision != HGKS_FP32) return fail(nullptr, HGKS_EINVAL, "bad precision");
   if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(nullptr, HGKS_EINVAL, "bad rank/nranks");
+  if (p->force_mode != HGKS_FORCE_NONE && p->force_mode != HGKS_FORCE_CONST && p->force_mode != HGKS_FORCE_BULK)
+    return fail(nullptr, HGKS_EINVAL, "bad force_mode");
+  if (p->force_mode != HGKS_FORCE_NONE && !std::isfinite(p->force)) return fail(nullptr, HGKS_EINVAL, "force not finite");
   if (p->nranks > 1 && !p->nccl_id) return fail(nullptr, HGKS_EINVAL, "nranks > 1 needs nccl_id");
   if (p->n[2] / p->nranks < 3) return fail(nullptr, HGKS_EINVAL, "nz/nranks < 3");
 
@@ -484,6 +528,8 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     free(hd);
     ok = ok && cudaMalloc(&c->diag_dev, (DIAG_BLOCKS + 1) * NDIAG * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->diag_host, NDIAG * sizeof(double)) == cudaSuccess;
+    const size_t ublocks = ((size_t)nloc[0] * nloc[1] * nloc[2] + DIAG_TPB - 1) / DIAG_TPB;
+    ok = ok && cudaMalloc(&c->bulk_dev, 2 * ublocks * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->metric, tot * c->esz) == cudaSuccess;
     if (ok) {
       if (c->fp32) {
@@ -511,6 +557,9 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   h.t = 0;
   h.dt_fixed = p->dt_fixed;
   h.cfl = p->cfl;
+  h.force_mode = (int)p->force_mode;
+  h.f_init = h.f_prev = h.force = p->force_mode == HGKS_FORCE_NONE ? 0.0 : p->force;
+  h.force_target = p->force_target;
   h.bad_cell = ~0ull;
   *c->ctl_host = h;
   if (cudaMemcpyAsync(c->ctl, c->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, c->s) != cudaSuccess ||
@@ -547,9 +596,19 @@ static int set_state_t(hgks_ctx* c) {
   const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   T* Q = (T*)c->Q[c->cur];
   pack_kernel<T><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>(c->stage64, Q, g);
+  int rc;
+  if (c->p.force_mode != HGKS_FORCE_NONE && (rc = diagnostics_t<T>(c))) return rc;  // bulk of Q^0 (O-27)
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
   CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  if (c->p.force_mode != HGKS_FORCE_NONE) {  // restart the controller from this state
+    const double* a = c->diag_host;
+    h->volume = a[HGKS_DIAG_VOLUME];
+    h->m_cur = a[HGKS_DIAG_MOM_X] / h->volume;
+    h->rho_cur = a[HGKS_DIAG_MASS] / h->volume;
+    h->hist = 0;
+    h->f_prev = h->force = c->p.force;
+  }
   h->red[0] = 0;
   h->red[1] = 0;
   h->bad_cell = ~0ull;
@@ -644,32 +703,6 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
 
 }  // extern "C"
 
-template <typename T>
-static int diagnostics_t(hgks_ctx* c) {
-  Geo<T> g = make_geo<T>(c);
-  T* Q = (T*)c->Q[c->cur];
-  // ghosts of the current state (a halted hgks_step leaves ctl->halt set, which gates the ghost
-  // kernels; hgks_step resets it on entry anyway)
-  CUDA_TRY(c, cudaMemsetAsync(&c->ctl->halt, 0, sizeof(int), c->s));
-  int rc;
-  if ((rc = fill_ghosts<T>(c, Q))) return rc;
-  DiagGeo dg;
-  const int nloc[3] = {c->n[0], c->n[1], c->nzl};
-  for (int d = 0, off = 0; d < 3; off += 2 * nloc[d], ++d) {
-    dg.jc[d] = c->dmetric + off;
-    dg.w[d] = c->dmetric + off + nloc[d];
-  }
-  double* out = c->diag_dev + DIAG_BLOCKS * NDIAG;
-  diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->diag_dev);
-  diag_final_kernel<NDIAG><<<1, DIAG_TPB, 0, c->s>>>(c->diag_dev, DIAG_BLOCKS, out);
-  c->total_launches += 2;
-  CUDA_TRY(c, cudaGetLastError());
-  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(out, out, NDIAG, ncclFloat64, ncclSum, c->comm, c->s));
-  CUDA_TRY(c, cudaMemcpyAsync(c->diag_host, out, NDIAG * sizeof(double), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
-  return HGKS_OK;
-}
-
 extern "C" {
 
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
@@ -691,6 +724,19 @@ int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
   return HGKS_OK;
 }
 
+int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* bulk_density) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_get_forcing: ctx is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  const bool b = c->p.force_mode == HGKS_FORCE_BULK;
+  if (force) *force = h->f_prev;
+  if (bulk_momentum) *bulk_momentum = b ? h->m_cur : 0.0;
+  if (bulk_density) *bulk_density = b ? h->rho_cur : 0.0;
+  return HGKS_OK;
+}
+
 int hgks_destroy(hgks_ctx* c) {
   if (!c) return HGKS_OK;
   cudaSetDevice(c->dev);
@@ -703,6 +749,7 @@ int hgks_destroy(hgks_ctx* c) {
   cudaFree(c->metric);
   cudaFree(c->dmetric);
   cudaFree(c->diag_dev);
+  cudaFree(c->bulk_dev);
   if (c->diag_host) cudaFreeHost(c->diag_host);
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->ev_in) cudaEventDestroy(c->ev_in);

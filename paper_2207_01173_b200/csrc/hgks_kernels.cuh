@@ -31,6 +31,14 @@ struct Ctl {
   int halt;                     // 0 running, 1 invalid state, 2 reached t_end
   int pending;                  // 1: a step has run and awaits commit
   long long steps_done;         // committed steps in the current hgks_step call
+  // streamwise body force (O-26, O-27; hgks_force_mode)
+  int force_mode;               // 0 none, 1 constant f, 2 dead-beat on the bulk momentum
+  int hist;                     // mode 2: 1 once a step has been committed since set_state
+  double force;                 // f of the step in flight
+  double f_init, force_target, volume;
+  double m_cur, rho_cur;        // bulk momentum / density of the committed state
+  double m_prev, dt_prev, f_prev;  // controller memory: previous step's m, dt and f
+  double bulk_new[2];           // (sum rho dV, sum rho U dV) of the newest state (allreduced)
 };
 
 template <typename T>
@@ -52,6 +60,32 @@ struct Geo {
   int wall[3];     // 1: isothermal no-slip walls at both ends of the axis (O-17)
   T T_wall;
 };
+
+constexpr int DIAG_TPB = 256;  // block size of the fixed-order reductions (update, diagnostics)
+
+// fp64 cell-centre metric J = d(index)/dx and cell widths of every axis (local cell index)
+struct DiagGeo {
+  const double* jc[3];
+  const double* w[3];
+};
+
+// sum v[0..N) over the block (fixed tree order); result valid in thread 0
+template <int N>
+__device__ __forceinline__ void block_sum_fixed(double (&v)[N], double* sh) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] = v[n];
+  __syncthreads();
+  for (int s = DIAG_TPB / 2; s > 0; s >>= 1) {
+    if (t < s) {
+#pragma unroll
+      for (int n = 0; n < N; ++n) sh[n * DIAG_TPB + t] += sh[n * DIAG_TPB + t + s];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) v[n] = sh[n * DIAG_TPB];
+}
 
 template <typename T>
 __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, int k) {
@@ -487,16 +521,22 @@ __device__ __forceinline__ void block_max_commit(double s, unsigned long long* d
 // ---- flux divergence + S2O4 stage update (Eqs. (3)-(4), (7)) ----------------------------------
 // STAGE 1: Qs = Q + dt/2 L + dt^2/8 dL ;  R = Q + dt L + dt^2/6 dL
 // STAGE 2: R  = R + dt^2/3 dL(Q*)  (= Q^{n+1}); epilogue: validity + wave speed into ctl->red
+// Body force (O-26; ctl->force_mode != 0): stage 1 adds S = (0, rho f, 0, 0, rho U f) to L and
+// f (L_rho, L_rhoU) to dL of (Q^n); stage 2 adds f (Lt_rho, Lt_rhoU) to dL(Q*) with
+// Lt = L + dt/2 dL of Q^n, recovered from the two stage-1 outputs: with a = Q* - Q^n and
+// b = R - Q^n (a = dt L/2 + dt^2 dL/8, b = dt L + dt^2 dL/6), Lt = (8a - 3b)/dt.  Mode 2 also
+// sums (rho dV, rho U dV) of Q^{n+1} per block (fixed order) into bulk[2 * blockIdx.x + {0, 1}].
 template <typename T, int STAGE>
-__global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
+__global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
-                              Geo<T> g, double gamma, Ctl* __restrict__ ctl) {
+                              Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk) {
   if (ctl->halt) return;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const long long ncell = (long long)nx * ny * nz;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const double dt = ctl->dt;
-  double smax = 0.0;
+  const int fmode = ctl->force_mode;
+  double smax = 0.0, bsum[2] = {0.0, 0.0};
   if (e < ncell) {
     const int i = (int)(e % nx);
     const int j = (int)((e / nx) % ny);
@@ -508,26 +548,51 @@ __global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __
     const long long oy = nx, oz = (long long)nx * ny;
     const T ihx = g.iw[0][i], ihy = g.iw[1][j], ihz = g.iw[2][k];
     const T tdt = T(dt);
-    T out[5];
+    T dL[5], L[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      const T dL = -((FX[(5 + c) * nfx + ix + 1] - FX[(5 + c) * nfx + ix]) * ihx +
-                     (FY[(5 + c) * nfy + iy + oy] - FY[(5 + c) * nfy + iy]) * ihy +
-                     (FZ[(5 + c) * nfz + iz + oz] - FZ[(5 + c) * nfz + iz]) * ihz);
-      const long long qi = qidx(g, c, i, j, k);
-      if (STAGE == 1) {
-        const T L = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * ihx + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * ihy +
-                      (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * ihz);
-        const T q = Q[qi];
-        Qs[qi] = q + T(0.5) * tdt * L + T(0.125) * tdt * tdt * dL;
-        R[qi] = q + tdt * L + (T(1) / T(6)) * tdt * tdt * dL;
-      } else {
-        const T v = R[qi] + (T(1) / T(3)) * tdt * tdt * dL;
+      dL[c] = -((FX[(5 + c) * nfx + ix + 1] - FX[(5 + c) * nfx + ix]) * ihx +
+                (FY[(5 + c) * nfy + iy + oy] - FY[(5 + c) * nfy + iy]) * ihy +
+                (FZ[(5 + c) * nfz + iz + oz] - FZ[(5 + c) * nfz + iz]) * ihz);
+      if (STAGE == 1)
+        L[c] = -((FX[c * nfx + ix + 1] - FX[c * nfx + ix]) * ihx + (FY[c * nfy + iy + oy] - FY[c * nfy + iy]) * ihy +
+                 (FZ[c * nfz + iz + oz] - FZ[c * nfz + iz]) * ihz);
+    }
+    if (STAGE == 1) {
+      T q[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) q[c] = Q[qidx(g, c, i, j, k)];
+      if (fmode) {  // O-26
+        const T f = T(ctl->force);
+        L[1] += q[0] * f;
+        L[4] += q[1] * f;
+        dL[1] += f * L[0];
+        dL[4] += f * L[1];
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const long long qi = qidx(g, c, i, j, k);
+        Qs[qi] = q[c] + T(0.5) * tdt * L[c] + T(0.125) * tdt * tdt * dL[c];
+        R[qi] = q[c] + tdt * L[c] + (T(1) / T(6)) * tdt * tdt * dL[c];
+      }
+    } else {
+      if (fmode) {  // O-26: Lt = L + dt/2 dL of Q^n = (8a - 3b)/dt
+        const double f = ctl->force;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const long long qi = qidx(g, c, i, j, k);
+          const double qn = (double)Q[qi], a = (double)Qs[qi] - qn, b = (double)R[qi] - qn;
+          dL[c == 0 ? 1 : 4] += T(f * (8.0 * a - 3.0 * b) / dt);
+        }
+      }
+      T out[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const long long qi = qidx(g, c, i, j, k);
+        const T v = R[qi] + (T(1) / T(3)) * tdt * tdt * dL[c];
         R[qi] = v;
         out[c] = v;
       }
-    }
-    if (STAGE == 2) {
       bool ok;
       smax = wave_speed(out, g, i, j, k, gamma, ok);
       if (!ok) {
@@ -536,9 +601,24 @@ __global__ void update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __
         atomicMin(&ctl->bad_cell, gid);
         ctl->red[1] = 1ull;  // benign race: every writer stores 1
       }
+      if (fmode == 2) {
+        const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
+        bsum[0] = (double)out[0] * vol;
+        bsum[1] = (double)out[1] * vol;
+      }
     }
   }
-  if (STAGE == 2) block_max_commit(smax, &ctl->red[0]);
+  if (STAGE == 2) {
+    block_max_commit(smax, &ctl->red[0]);
+    if (fmode == 2) {  // uniform branch: every thread of the block takes it
+      __shared__ double sh[2 * DIAG_TPB];
+      block_sum_fixed(bsum, sh);
+      if (threadIdx.x == 0) {
+        bulk[2 * blockIdx.x] = bsum[0];
+        bulk[2 * blockIdx.x + 1] = bsum[1];
+      }
+    }
+  }
 }
 
 // ---- wave-speed max / validity of the current state (set_state) ------------------------------
@@ -577,6 +657,14 @@ __device__ __forceinline__ void commit_pending(Ctl* c) {
   c->dt_last = c->dt;
   c->steps_done += 1;
   c->smax_cur = c->red[0];
+  c->f_prev = c->force;
+  if (c->force_mode == 2) {
+    c->m_prev = c->m_cur;
+    c->dt_prev = c->dt;
+    c->m_cur = c->bulk_new[1] / c->volume;
+    c->rho_cur = c->bulk_new[0] / c->volume;
+    c->hist = 1;
+  }
 }
 
 __global__ void dt_kernel(Ctl* c) {
@@ -594,6 +682,12 @@ __global__ void dt_kernel(Ctl* c) {
     if (dt > rem) dt = rem;
   }
   c->dt = dt;
+  if (c->force_mode == 1) {
+    c->force = c->f_init;
+  } else if (c->force_mode == 2) {  // O-27
+    c->force = c->hist ? c->f_prev + ((c->force_target - c->m_cur) / dt - (c->m_cur - c->m_prev) / c->dt_prev) / c->rho_cur
+                       : c->f_prev + (c->force_target - c->m_cur) / (dt * c->rho_cur);
+  }
   c->red[0] = 0ull;
   c->red[1] = 0ull;
   c->pending = 1;

@@ -24,11 +24,12 @@ HGKS_FP64, HGKS_FP32 = 0, 1
 HGKS_PERIODIC, HGKS_WALL_ISOTHERMAL = 0, 1
 HGKS_UNIFORM, HGKS_TANH = 0, 1
 HGKS_MU_CONST, HGKS_MU_POWER = 0, 1
+HGKS_FORCE_NONE, HGKS_FORCE_CONST, HGKS_FORCE_BULK = 0, 1, 2
 KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt", "recon")
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_diagnostics", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+            "hgks_diagnostics", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
 DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
 
 
@@ -45,7 +46,8 @@ class Params(C.Structure):
                 ("mu_law", C.c_int), ("mu_ref", C.c_double), ("T_ref", C.c_double),
                 ("omega", C.c_double), ("T_wall", C.c_double), ("cfl", C.c_double), ("dt_fixed", C.c_double),
                 ("precision", C.c_int), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("device", C.c_int32), ("nccl_id", C.c_void_p), ("stream", C.c_void_p)]
+                ("device", C.c_int32), ("nccl_id", C.c_void_p), ("stream", C.c_void_p),
+                ("force_mode", C.c_int), ("force", C.c_double), ("force_target", C.c_double)]
 
 
 class HaloPlan(C.Structure):
@@ -79,6 +81,7 @@ def lib():
         L.hgks_slab_of.argtypes = [C.c_int32] * 3 + [C.POINTER(C.c_int32)] * 2
         L.hgks_make_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(HaloPlan)]
         L.hgks_diagnostics.argtypes = [vp, C.c_double, _dp]
+        L.hgks_get_forcing.argtypes = [vp, _dp, _dp, _dp]
         L.hgks_profile_enable.argtypes = [vp, C.c_int]
         L.hgks_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.hgks_test_gp_flux.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
@@ -121,7 +124,8 @@ def hgks_get_nccl_id() -> bytes:
 def make_params(n, lo, hi, gamma=1.4, mu=0.0, prandtl=1.0, mu_law=HGKS_MU_CONST, T_ref=1.0,
                 omega=0.0, cfl=0.4, dt_fixed=0.0, precision=HGKS_FP64, rank=0, nranks=1,
                 device=0, nccl_id=None, stream=None, bc=(HGKS_PERIODIC,) * 3,
-                stretch=(HGKS_UNIFORM,) * 3, stretch_b=(0.0, 0.0, 0.0), T_wall=1.0):
+                stretch=(HGKS_UNIFORM,) * 3, stretch_b=(0.0, 0.0, 0.0), T_wall=1.0,
+                force_mode=HGKS_FORCE_NONE, force=0.0, force_target=0.0):
     p = Params()
     for d in range(3):
         p.n[d] = int(n[d])
@@ -137,6 +141,7 @@ def make_params(n, lo, hi, gamma=1.4, mu=0.0, prandtl=1.0, mu_law=HGKS_MU_CONST,
     p._id_buf = C.create_string_buffer(nccl_id, len(nccl_id)) if nccl_id is not None else None
     p.nccl_id = C.cast(p._id_buf, C.c_void_p) if nccl_id is not None else None
     p.stream = stream
+    p.force_mode, p.force, p.force_target = int(force_mode), float(force), float(force_target)
     return p
 
 
@@ -190,6 +195,13 @@ def hgks_diagnostics(ctx, rho0: float = 1.0) -> np.ndarray:
     out = np.zeros(len(DIAG_NAMES))
     _check(lib().hgks_diagnostics(ctx, rho0, out.ctypes.data_as(_dp)), ctx)
     return out
+
+
+def hgks_get_forcing(ctx):
+    """(f of the last committed step, bulk momentum m, bulk density rho_b) of the current state."""
+    f, m, r = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().hgks_get_forcing(ctx, C.byref(f), C.byref(m), C.byref(r)), ctx)
+    return f.value, m.value, r.value
 
 
 def hgks_profile_enable(ctx, enable: bool = True) -> None:
