@@ -876,3 +876,30 @@ void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double
   out[OR_DIAG_EPS_S] = g->mu_ref * acc[OR_DIAG_EPS_S] / (rho0 * omega);
   out[OR_DIAG_EPS_D] = 4.0 / 3.0 * g->mu_ref * acc[OR_DIAG_EPS_D] / (rho0 * omega);
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Plane statistics of the channel: raw moments of the state averaged over the x-z
+ * plane of every y index j (the paper's <.> is the mean over time and the X and Z directions,
+ * P:1190-1191; time averaging is done by the caller over samples).  Per plane, in this order:
+ *   rho, U, V, W, U^2, V^2, W^2, UV, rho U, rho V, rho U V, c, M, M^2, T, p
+ * with c = sqrt(gamma p / rho) the local sound speed, M = |U| / c, T = p / rho (O-28).
+ * out[j * OR_NSTAT + s] = (1/(nx nz)) sum_{i,k} of moment s (x and z are uniform axes).
+ * ---------------------------------------------------------------------------------------- */
+void or_plane_stats(const or_gas* g, const or_grid* gr, const double* q, double* out) {
+  int nx = gr->n[0], ny = gr->n[1], nz = gr->n[2];
+  for (int j = 0; j < ny; ++j) {
+    double acc[OR_NSTAT] = {0};
+    for (int k = 0; k < nz; ++k)
+      for (int i = 0; i < nx; ++i) {
+        double rho = q[cidx(gr, 0, i, j, k)];
+        double U = q[cidx(gr, 1, i, j, k)] / rho, V = q[cidx(gr, 2, i, j, k)] / rho, W = q[cidx(gr, 3, i, j, k)] / rho;
+        double p = (g->gamma - 1.0) * (q[cidx(gr, 4, i, j, k)] - 0.5 * rho * (U * U + V * V + W * W));
+        double c = sqrt(g->gamma * p / rho);
+        double M = sqrt(U * U + V * V + W * W) / c;
+        double v[OR_NSTAT] = {rho, U, V, W, U * U, V * V, W * W, U * V, rho * U, rho * V, rho * U * V,
+                              c, M, M * M, p / rho, p};
+        for (int s = 0; s < OR_NSTAT; ++s) acc[s] += v[s];
+      }
+    for (int s = 0; s < OR_NSTAT; ++s) out[(long)j * OR_NSTAT + s] = acc[s] / ((double)nx * nz);
+  }
+}

@@ -151,6 +151,13 @@ typedef struct {
 int or_run_forced(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_fixed, double cfl,
                   const or_forcing* fc, double* dt_hist, double* f_hist);
 
+/* x-z plane means of 16 raw moments for every y index (channel statistics, O-28):
+ * rho, U, V, W, U^2, V^2, W^2, UV, rho U, rho V, rho U V, c, M, M^2, T, p ; q unghosted
+ * [5][nz][ny][nx]; out[ny][OR_NSTAT].  Pins (test_oracle_stats.py): plane means of fields built
+ * from x/z harmonics, whose exact means follow from the discrete orthogonality of the harmonics. */
+#define OR_NSTAT 16
+void or_plane_stats(const or_gas* g, const or_grid* gr, const double* q, double* out);
+
 /* Number of OpenMP threads the oracle uses (1 when built without OpenMP). */
 /* Volume diagnostics of a ghosted block (ghosts filled): E_k, enstrophy (O-24),
  * the two terms of eps_com (mu = mu_ref), and conservation monitors; velocity

@@ -84,6 +84,7 @@ def lib():
                              C.c_double, _dp]
         L.or_run_forced.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_int, C.c_double, C.c_double,
                                     C.POINTER(Forcing), _dp, _dp]
+        L.or_plane_stats.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, _dp]
         L.or_diagnostics.argtypes = [C.POINTER(Gas), C.POINTER(Grid), _dp, C.c_double, _dp]
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -290,6 +291,18 @@ def run_forced(gas: Gas, q: np.ndarray, dx, nsteps: int, mode: int, force: float
     if rc:
         raise ValueError("oracle run hit an invalid state")
     return q, hist[:nsteps], fh[:nsteps]
+
+
+STAT_NAMES = ("rho", "U", "V", "W", "UU", "VV", "WW", "UV", "rhoU", "rhoV", "rhoUV", "c", "M", "MM", "T", "p")
+
+
+def plane_stats(gas: Gas, q: np.ndarray, dx=None, grid: Grid | None = None) -> np.ndarray:
+    """or_plane_stats: [ny][16] x-z plane means in STAT_NAMES order."""
+    q = _arr(q)
+    gr = _grid_of(q, dx, grid)
+    out = np.zeros((q.shape[2], len(STAT_NAMES)))
+    lib().or_plane_stats(C.byref(gas), C.byref(gr), _p(q), _p(out))
+    return out
 
 
 def num_threads() -> int:
