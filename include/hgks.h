@@ -144,6 +144,20 @@ typedef enum {
 } hgks_diag;
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]);
 
+/* x-z plane means of the current state for every GLOBAL y index j (channel statistics, P:1186-1238;
+ * the paper's <.> averages over time and the X and Z directions, P:1190-1191 -- time averaging is
+ * left to the caller, who samples this every few steps).  out[j * HGKS_STAT_COUNT + s], j < ny,
+ * s in hgks_stat order; c = sqrt(gamma p / rho), M = |U| / c, T = p / rho (reading O-28).  fp64 for
+ * either precision; one block per plane with a fixed summation order, then an NCCL sum over the z
+ * slabs.  Collective; synchronises.  Errors: HGKS_EINVAL (NULL, no state), ECUDA, ENCCL. */
+#define HGKS_STAT_COUNT 16
+typedef enum {
+  HGKS_STAT_RHO = 0, HGKS_STAT_U, HGKS_STAT_V, HGKS_STAT_W, HGKS_STAT_UU, HGKS_STAT_VV, HGKS_STAT_WW,
+  HGKS_STAT_UV, HGKS_STAT_RHOU, HGKS_STAT_RHOV, HGKS_STAT_RHOUV, HGKS_STAT_C, HGKS_STAT_M,
+  HGKS_STAT_MM, HGKS_STAT_T, HGKS_STAT_P
+} hgks_stat;
+int hgks_plane_stats(hgks_ctx* c, double* out);
+
 /* Streamwise force state (collective, synchronises): *force = f applied in the last committed step
  * (the params' force before the first step); *bulk_momentum, *bulk_density = m and rho_b of the
  * current state (HGKS_FORCE_BULK; 0 otherwise).  Any output pointer may be NULL. */

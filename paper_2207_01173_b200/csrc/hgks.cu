@@ -66,6 +66,7 @@ struct hgks_ctx {
   double* dmetric = nullptr;  // fp64 per axis: J at the cell centres [n], cell widths [n] (diagnostics)
   double* diag_dev = nullptr; // DIAG_BLOCKS * NDIAG block partials, then NDIAG results
   double* diag_host = nullptr;  // pinned NDIAG
+  double* stats_dev = nullptr;  // ny * NSTAT plane sums (hgks_plane_stats)
   double* bulk_dev = nullptr;   // 2 per update block: (sum rho dV, sum rho U dV) partials (O-27)
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
@@ -530,6 +531,7 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     ok = ok && cudaMallocHost(&c->diag_host, NDIAG * sizeof(double)) == cudaSuccess;
     const size_t ublocks = ((size_t)nloc[0] * nloc[1] * nloc[2] + DIAG_TPB - 1) / DIAG_TPB;
     ok = ok && cudaMalloc(&c->bulk_dev, 2 * ublocks * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->stats_dev, (size_t)nloc[1] * NSTAT * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->metric, tot * c->esz) == cudaSuccess;
     if (ok) {
       if (c->fp32) {
@@ -724,6 +726,34 @@ int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
   return HGKS_OK;
 }
 
+}  // extern "C"
+
+template <typename T>
+static int plane_stats_t(hgks_ctx* c, double* out) {
+  Geo<T> g = make_geo<T>(c);
+  plane_stats_kernel<T><<<c->n[1], DIAG_TPB, 0, c->s>>>((const T*)c->Q[c->cur], g, c->p.gamma, c->stats_dev);
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  const size_t cnt = (size_t)c->n[1] * NSTAT;
+  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(c->stats_dev, c->stats_dev, cnt, ncclFloat64, ncclSum, c->comm, c->s));
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->stats_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  const double inv = 1.0 / ((double)c->n[0] * c->n[2]);
+  for (size_t k = 0; k < cnt; ++k) out[k] *= inv;
+  return HGKS_OK;
+}
+
+extern "C" {
+
+int hgks_plane_stats(hgks_ctx* c, double* out) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_plane_stats: ctx is NULL");
+  if (!out) return fail(c, HGKS_EINVAL, "hgks_plane_stats: out is NULL");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_plane_stats: no state set");
+  static_assert(HGKS_STAT_COUNT == NSTAT, "statistic count");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  return c->fp32 ? plane_stats_t<float>(c, out) : plane_stats_t<double>(c, out);
+}
+
 int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* bulk_density) {
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_get_forcing: ctx is NULL");
   CUDA_TRY(c, cudaSetDevice(c->dev));
@@ -750,6 +780,7 @@ int hgks_destroy(hgks_ctx* c) {
   cudaFree(c->dmetric);
   cudaFree(c->diag_dev);
   cudaFree(c->bulk_dev);
+  cudaFree(c->stats_dev);
   if (c->diag_host) cudaFreeHost(c->diag_host);
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->ev_in) cudaEventDestroy(c->ev_in);

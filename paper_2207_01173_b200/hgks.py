@@ -29,7 +29,8 @@ KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt",
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_diagnostics", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+            "hgks_diagnostics", "hgks_plane_stats", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+STAT_NAMES = ("rho", "U", "V", "W", "UU", "VV", "WW", "UV", "rhoU", "rhoV", "rhoUV", "c", "M", "MM", "T", "p")
 DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
 
 
@@ -82,6 +83,7 @@ def lib():
         L.hgks_make_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(HaloPlan)]
         L.hgks_diagnostics.argtypes = [vp, C.c_double, _dp]
         L.hgks_get_forcing.argtypes = [vp, _dp, _dp, _dp]
+        L.hgks_plane_stats.argtypes = [vp, _dp]
         L.hgks_profile_enable.argtypes = [vp, C.c_int]
         L.hgks_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.hgks_test_gp_flux.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
@@ -197,6 +199,13 @@ def hgks_diagnostics(ctx, rho0: float = 1.0) -> np.ndarray:
     return out
 
 
+def hgks_plane_stats(ctx, ny: int) -> np.ndarray:
+    """[ny][16] x-z plane means of the current state (STAT_NAMES order); collective."""
+    out = np.zeros((ny, len(STAT_NAMES)))
+    _check(lib().hgks_plane_stats(ctx, out.ctypes.data_as(_dp)), ctx)
+    return out
+
+
 def hgks_get_forcing(ctx):
     """(f of the last committed step, bulk momentum m, bulk density rho_b) of the current state."""
     f, m, r = C.c_double(), C.c_double(), C.c_double()
@@ -263,6 +272,9 @@ class Solver:
     def step(self, nsteps: int = 1, t_end: float = 0.0):
         self.t, dt = hgks_step(self.ctx, nsteps, self.t, t_end)
         return dt
+
+    def plane_stats(self) -> np.ndarray:
+        return hgks_plane_stats(self.ctx, self.n[1])
 
     def diagnostics(self, rho0: float = 1.0) -> dict:
         return dict(zip(DIAG_NAMES, hgks_diagnostics(self.ctx, rho0)))
