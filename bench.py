@@ -210,7 +210,9 @@ def main():
                             bc=(H.HGKS_PERIODIC, H.HGKS_WALL_ISOTHERMAL, H.HGKS_PERIODIC),
                             stretch=(H.HGKS_UNIFORM, H.HGKS_TANH, H.HGKS_UNIFORM), stretch_b=(0.0, chp["b_g"], 0.0),
                             cfl=0.4, precision=precision, rank=rank, nranks=ws, device=local, nccl_id=nccl_id,
-                            stream=stream.cuda_stream)
+                            stream=stream.cuda_stream,
+                            # constant bulk momentum rho_b U_b = 1 (units of the channel, O-27)
+                            force_mode=H.HGKS_FORCE_BULK, force=0.0, force_target=1.0)
         return H.Solver(grid, lo, hi, mu=prm["mu"], cfl=0.4, precision=precision, rank=rank, nranks=ws,
                         device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
 
@@ -308,7 +310,8 @@ def main():
         "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": ("channel_" + "x".join(map(str, grid))) if channel else (f"tgv{n}" + ("_weak" if args.weak else "")),
                    "grid": list(grid), "precision": "fp64",
-                   "mode": "cfl 0.4 (dt allreduce each step)", "decomposition": f"z-slab x{ws}",
+                   "mode": "cfl 0.4 (dt allreduce each step)" + (", bulk-momentum forcing (O-27)" if channel else ""),
+                   "decomposition": f"z-slab x{ws}",
                    "l2": "inputs larger than L2 (one state = %d MB)" % (5 * grid[0] * grid[1] * grid[2] * 8 // 2**20)},
         "clocks": clk,
         "gpu_launches": int(r64["total_launches"]),
