@@ -49,8 +49,9 @@ def main(tag, n):
                       f"{m.get('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active', 0):.1f} | "
                       f"{m['dram__bytes_read.sum'] / 1e6:.0f} | {m['dram__bytes_write.sum'] / 1e6:.0f} |")
         for stage in (1, 2):
-            ks = [v for k, vs in per.items() for v in vs if k.startswith("hgks::flux_kernel") or k.startswith("flux_kernel")]
-            ks = [v for k, vs in per.items() if "flux_kernel" in k and k.rstrip(">").endswith(f", {stage}") for v in vs]
+            # flux_kernel<T, DIR, STAGE[, PRF]>: the stage is the third template argument
+            ks = [v for k, vs in per.items() if "flux_kernel" in k
+                  and k.split("<", 1)[1].rstrip(">").split(",")[2].strip() == str(stage) for v in vs]
             if ks:
                 flop = sum(v["flop"] for v in ks) / len(ks)
                 out[f"{prec}_flop_per_face_stage{stage}"] = flop / faces("flux", n)
