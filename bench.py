@@ -251,6 +251,19 @@ def main():
         rate = cells * args.steps / (ms / 1000.0)
         res = dict(ms_per_step=ms / args.steps, value=rate, clocks=clk.summary(), ms_k=ms_k, launches=launches,
                    total_launches=total_launches, t=s.t)
+        # NEXT-1/2 device reductions outside the timed step (synchronous calls, events on the stream)
+        aux = {}
+        for name, fn in (("diagnostics", lambda: H.hgks_diagnostics(s.ctx)),
+                         ("plane_stats", lambda: H.hgks_plane_stats(s.ctx, grid[1]))):
+            fn()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(3):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            aux[name + "_ms"] = a0.elapsed_time(a1) / 3
+        res["aux"] = aux
         # e2e through the public API with host buffers (pinned): H2D state, step, D2H state per step
         if not args.no_e2e:
             qh = torch.from_numpy(q).pin_memory()
@@ -321,6 +334,7 @@ def main():
                          "achieved_gbs": r64["value"] / ws * alg_bytes / 1e9, "peak_gbs": hbm,
                          "frac": r64["value"] / ws * alg_bytes / 1e9 / hbm},
         "kernel_ms_per_step": {k: v / args.steps for k, v in r64["ms_k"].items()},
+        "aux_ms": r64.get("aux"),
     }
     if "e2e" in r64:
         line["e2e"] = r64["e2e"]
