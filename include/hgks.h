@@ -87,10 +87,21 @@ typedef struct {
   hgks_force_mode force_mode; /* streamwise body force (see hgks_force_mode); NONE for TGV           */
   double force;          /* CONST: the acceleration f; BULK: f before the first step (f_init)      */
   double force_target;   /* BULK: target bulk momentum m_b (e.g. rho_b U_b = 1 for the channel)    */
+  int64_t group_key;     /* nranks > 1 without NCCL: != 0 joins the in-process LOOPBACK group of
+                            that key (nccl_id must be NULL).  The nranks contexts of the group live
+                            in ONE process, each driven by its own host thread, and may share one
+                            device: halos move by device-to-device copies ordered with CUDA events,
+                            reductions run in a fixed rank order on the device, and the collective
+                            calls synchronise the threads with a host barrier (120 s timeout ->
+                            HGKS_ENCCL).  Same kernels, slab split and halo plan as the NCCL path:
+                            it exists so the decomposition can be verified on a single GPU
+                            (decomposition invariance, SURVEY O-P15).  nranks <= 16.  0: unused.  */
 } hgks_params;
 
-/* Validate p, allocate device memory, create streams and (nranks > 1) the NCCL communicator.
- * *out receives the context, or NULL on failure.  Errors: EINVAL, ECUDA, ENCCL, ENOMEM. */
+/* Validate p, allocate device memory, create streams and (nranks > 1) the NCCL communicator, or
+ * join the loopback group (group_key; returns once all nranks members have joined).
+ * *out receives the context, or NULL on failure.  Errors: EINVAL, ECUDA, ENCCL (NCCL init failure
+ * or loopback group timeout / inconsistent nranks), ENOMEM. */
 int hgks_create(const hgks_params* p, hgks_ctx** out);
 
 /* This rank's slab: global z planes [z_begin, z_begin + nz_local).  Planes are split as evenly as
@@ -104,7 +115,9 @@ int hgks_local_extent(const hgks_ctx* c, int32_t* z_begin, int32_t* nz_local);
 int hgks_set_state(hgks_ctx* c, const double* q, int on_device);
 
 /* Advance up to nsteps S2O4 steps.  dt per step is dt_fixed, or the CFL value from
- * the global max wave speed (one 8-byte NCCL max-allreduce per step).  If t_end > 0 the last dt
+ * the global max wave speed (one 8-byte NCCL max-allreduce per step).  Each stage's z halo (Alg. 2,
+ * P:497-521) runs on a high-priority communication stream while the x-direction reconstruction of
+ * the interior z planes proceeds; only the ghost-plane lines wait for it.  If t_end > 0 the last dt
  * is clamped so t does not pass t_end and the call stops there.  *t_inout is read (start time)
  * and written (time reached); *dt_last (may be NULL) receives the last dt taken.  All steps are
  * enqueued without host round trips; the call reads one status word at the end.

@@ -7,12 +7,17 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hgks.h"
 #include "../../include/hgks_test.h"
@@ -47,6 +52,8 @@ struct Prof {
   long long launches[HGKS_K_COUNT] = {0};
 };
 
+struct LoopGroup;
+
 }  // namespace
 
 struct hgks_ctx {
@@ -71,7 +78,14 @@ struct hgks_ctx {
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
   cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
+  cudaStream_t sc = nullptr;          // communication stream (high priority): the z halo of each stage
   cudaEvent_t ev_in = nullptr, ev_rec[3] = {}, ev_flux[3] = {};
+  cudaEvent_t ev_xy = nullptr;        // x/y ghosts of the stage input written (halo may start)
+  cudaEvent_t ev_halo = nullptr;      // z ghosts of the stage input landed
+  // loopback group (params.group_key): ordering events of the halo copies and the reductions
+  cudaEvent_t lb_post = nullptr, lb_done = nullptr, lb_rpost = nullptr, lb_rdone = nullptr;
+  LoopGroup* grp = nullptr;
+  void* red_tmp = nullptr;            // loopback reduction result before the in-place write-back
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;    // pinned
@@ -206,9 +220,182 @@ static GasK<T> make_gas(const hgks_params& p) {
 
 static int blocks_for(long long n, int tpb) { return (int)std::min<long long>((n + tpb - 1) / tpb, 148LL * 64); }
 
-// ---- ghost layers: x/y periodic kernel, then z by local copy (1 rank) or NCCL (slab halo) ----
+// ---- collectives: NCCL (one process per GPU) or the in-process loopback group --------------------
+// The loopback group (params.group_key) runs nranks contexts of one process, one host thread each,
+// possibly on one device.  A collective = publish (pointer + event recorded on the caller's
+// stream) -> host barrier -> every rank's stream waits on the peers' events and reads their
+// buffers -> completion event -> host barrier -> every rank's stream waits on the peers'
+// completion events, so no rank overwrites a buffer a peer is still reading.
+namespace {
+
+constexpr int LB_MAX = 16;
+constexpr double LB_TIMEOUT_S = 120.0;
+
+struct LoopGroup {
+  int n = 0, joined = 0, refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  hgks_ctx* m[LB_MAX] = {};
+  const void* ptr[LB_MAX] = {};
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::duration<double>(LB_TIMEOUT_S), [&] { return gen != g; });
+  }
+};
+
+std::mutex g_groups_mu;
+std::map<long long, LoopGroup*> g_groups;
+
+struct LbPtrs {
+  const void* p[LB_MAX];
+};
+
+// out[k] = op over ranks r = 0..n-1 (fixed order) of src_r[k]; op 0: max of u64, 1: sum of f64
+__global__ void lb_reduce_kernel(LbPtrs src, int n, long long count, int op, void* out) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < count; k += (long long)gridDim.x * blockDim.x) {
+    if (op == 0) {
+      unsigned long long v = 0;
+      for (int r = 0; r < n; ++r) v = max(v, ((const unsigned long long*)src.p[r])[k]);
+      ((unsigned long long*)out)[k] = v;
+    } else {
+      double v = 0.0;
+      for (int r = 0; r < n; ++r) v += ((const double*)src.p[r])[k];
+      ((double*)out)[k] = v;
+    }
+  }
+}
+
+}  // namespace
+
+static int lb_barrier(hgks_ctx* c) {
+  if (!c->grp->barrier()) return fail(c, HGKS_ENCCL, "loopback group: barrier timed out after %.0f s", LB_TIMEOUT_S);
+  return HGKS_OK;
+}
+
+// in-place allreduce of count elements of buf (device) on stream c->s; op 0: max u64, 1: sum f64
+static int coll_allreduce(hgks_ctx* c, void* buf, size_t count, int op) {
+  if (c->p.nranks == 1) return HGKS_OK;
+  if (c->comm) {
+    NCCL_TRY(c, ncclAllReduce(buf, buf, count, op == 0 ? ncclUint64 : ncclFloat64, op == 0 ? ncclMax : ncclSum, c->comm, c->s));
+    return HGKS_OK;
+  }
+  LoopGroup* G = c->grp;
+  const int r = c->p.rank, n = c->p.nranks;
+  int rc;
+  CUDA_TRY(c, cudaEventRecord(c->lb_rpost, c->s));
+  G->ptr[r] = buf;
+  if ((rc = lb_barrier(c))) return rc;
+  LbPtrs src{};
+  for (int q = 0; q < n; ++q) {
+    src.p[q] = G->ptr[q];
+    if (q != r) CUDA_TRY(c, cudaStreamWaitEvent(c->s, G->m[q]->lb_rpost, 0));
+  }
+  lb_reduce_kernel<<<(int)std::min<size_t>((count + 255) / 256, 64), 256, 0, c->s>>>(src, n, (long long)count, op, c->red_tmp);
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaEventRecord(c->lb_rdone, c->s));
+  if ((rc = lb_barrier(c))) return rc;
+  for (int q = 0; q < n; ++q)
+    if (q != r) CUDA_TRY(c, cudaStreamWaitEvent(c->s, G->m[q]->lb_rdone, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(buf, c->red_tmp, count * 8, cudaMemcpyDeviceToDevice, c->s));
+  return HGKS_OK;
+}
+
+// z halo of the ghosted state q (elements of esz bytes) on the communication stream c->sc, which
+// has already waited for the x/y ghosts (ev_xy).  Records ev_halo when the ghost planes landed.
+static int coll_halo(hgks_ctx* c, void* q, size_t esz) {
+  const hgks_halo_plan& pl = c->plan;
+  char* b = (char*)q;
+  const size_t bytes = (size_t)pl.count * esz;
+  if (c->p.nranks == 1) {  // periodic wrap within the slab
+    CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_down * esz, b + pl.send_up * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
+    CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_up * esz, b + pl.send_down * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
+  } else if (c->comm) {  // one grouped send/recv per neighbour (Alg. 2; O-22: no ordering needed)
+    ncclDataType_t ty = esz == 8 ? ncclFloat64 : ncclFloat32;
+    NCCL_TRY(c, ncclGroupStart());
+    NCCL_TRY(c, ncclSend(b + pl.send_up * esz, pl.count, ty, pl.up, c->comm, c->sc));
+    NCCL_TRY(c, ncclRecv(b + pl.recv_down * esz, pl.count, ty, pl.down, c->comm, c->sc));
+    NCCL_TRY(c, ncclSend(b + pl.send_down * esz, pl.count, ty, pl.down, c->comm, c->sc));
+    NCCL_TRY(c, ncclRecv(b + pl.recv_up * esz, pl.count, ty, pl.up, c->comm, c->sc));
+    NCCL_TRY(c, ncclGroupEnd());
+  } else {  // loopback: pull both ghost chunks from the neighbours' buffers
+    LoopGroup* G = c->grp;
+    const int r = c->p.rank;
+    int rc;
+    CUDA_TRY(c, cudaEventRecord(c->lb_post, c->sc));
+    G->ptr[r] = q;
+    if ((rc = lb_barrier(c))) return rc;
+    hgks_ctx* dn = G->m[pl.down];
+    hgks_ctx* up = G->m[pl.up];
+    CUDA_TRY(c, cudaStreamWaitEvent(c->sc, dn->lb_post, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->sc, up->lb_post, 0));
+    const char* bd = (const char*)G->ptr[pl.down];
+    const char* bu = (const char*)G->ptr[pl.up];
+    CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_down * esz, bd + dn->plan.send_up * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
+    CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_up * esz, bu + up->plan.send_down * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
+    CUDA_TRY(c, cudaEventRecord(c->lb_done, c->sc));
+    if ((rc = lb_barrier(c))) return rc;
+    CUDA_TRY(c, cudaStreamWaitEvent(c->sc, dn->lb_done, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->sc, up->lb_done, 0));
+  }
+  CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->sc));
+  return HGKS_OK;
+}
+
+// join (or create) the loopback group of the context's key; returns once all ranks have joined
+static int lb_join(hgks_ctx* c) {
+  const long long key = (long long)c->p.group_key;
+  LoopGroup* G;
+  {
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    auto it = g_groups.find(key);
+    if (it == g_groups.end()) {
+      G = new LoopGroup();
+      G->n = c->p.nranks;
+      g_groups[key] = G;
+    } else {
+      G = it->second;
+    }
+    if (G->n != c->p.nranks) return fail(c, HGKS_ENCCL, "loopback group %lld: nranks %d != %d", key, c->p.nranks, G->n);
+    if (G->m[c->p.rank]) return fail(c, HGKS_ENCCL, "loopback group %lld: rank %d joined twice", key, c->p.rank);
+    G->m[c->p.rank] = c;
+    G->refs += 1;
+    c->grp = G;
+  }
+  return lb_barrier(c);
+}
+
+static void lb_leave(hgks_ctx* c) {
+  LoopGroup* G = c->grp;
+  if (!G) return;
+  std::lock_guard<std::mutex> lk(g_groups_mu);
+  G->m[c->p.rank] = nullptr;
+  if (--G->refs == 0) {
+    for (auto it = g_groups.begin(); it != g_groups.end(); ++it)
+      if (it->second == G) {
+        g_groups.erase(it);
+        break;
+      }
+    delete G;
+  }
+  c->grp = nullptr;
+}
+
+// ---- ghost layers: x/y periodic / wall kernels on the compute stream, then the z halo (local
+// periodic copy, NCCL, or loopback) on the communication stream c->sc -> ev_halo.  With
+// wait_halo the compute stream waits for the halo; flux_sweeps instead lets the interior lines
+// of the first reconstruction sweep run while the halo is in flight.
 template <typename T>
-static int fill_ghosts(hgks_ctx* c, T* q) {
+static int fill_ghosts(hgks_ctx* c, T* q, bool wait_halo) {
   Geo<T> g = make_geo<T>(c);
   long long total = (long long)g.n[2] * g.plane;
   prof_begin(c, HGKS_K_GHOST);
@@ -221,22 +408,13 @@ static int fill_ghosts(hgks_ctx* c, T* q) {
   prof_end(c, HGKS_K_GHOST);
   c->total_launches += 1;
   CUDA_TRY(c, cudaGetLastError());
-  const hgks_halo_plan& pl = c->plan;
-  prof_begin(c, HGKS_K_HALO);
-  if (c->p.nranks == 1) {
-    size_t bytes = (size_t)pl.count * sizeof(T);
-    CUDA_TRY(c, cudaMemcpyAsync(q + pl.recv_down, q + pl.send_up, bytes, cudaMemcpyDeviceToDevice, c->s));
-    CUDA_TRY(c, cudaMemcpyAsync(q + pl.recv_up, q + pl.send_down, bytes, cudaMemcpyDeviceToDevice, c->s));
-  } else {
-    ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-    NCCL_TRY(c, ncclGroupStart());
-    NCCL_TRY(c, ncclSend(q + pl.send_up, pl.count, ty, pl.up, c->comm, c->s));
-    NCCL_TRY(c, ncclRecv(q + pl.recv_down, pl.count, ty, pl.down, c->comm, c->s));
-    NCCL_TRY(c, ncclSend(q + pl.send_down, pl.count, ty, pl.down, c->comm, c->s));
-    NCCL_TRY(c, ncclRecv(q + pl.recv_up, pl.count, ty, pl.up, c->comm, c->s));
-    NCCL_TRY(c, ncclGroupEnd());
-  }
-  prof_end(c, HGKS_K_HALO);
+  CUDA_TRY(c, cudaEventRecord(c->ev_xy, c->s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->sc, c->ev_xy, 0));
+  prof_begin(c, HGKS_K_HALO, c->sc);
+  int rc = coll_halo(c, q, sizeof(T));
+  prof_end(c, HGKS_K_HALO, c->sc);
+  if (rc) return rc;
+  if (wait_halo) CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_halo, 0));
   return HGKS_OK;
 }
 
@@ -258,20 +436,39 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     attr_done[pi][STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  auto recon_blocks = [&](int n1, int n2) { return (int)((5LL * (n1 + 4) * (n2 + 4) + 127) / 128); };
   // Two streams: the reconstruction sweep of direction d+1 (memory-bound) runs on s2 while the
   // flux sweep of direction d (FP64-bound) runs on s.  FF[d % 2] is written by recon d and read
   // by flux d; recon d+2 waits for flux d before reusing the buffer.
-  CUDA_TRY(c, cudaEventRecord(c->ev_in, c->s));  // stage input ready (ghosts filled)
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_in, 0));
+  // stage input: x/y ghosts written (ev_xy, recorded by fill_ghosts on c->s); z ghosts land on
+  // c->sc (ev_halo).  The x sweep's face lines of the interior z planes need no z ghost, so they
+  // run while the halo is in flight; its ghost-plane lines (z = -2, -1, nz, nz+1) and every
+  // later sweep wait for ev_halo.
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_xy, 0));
   const int n3[3] = {nx, ny, nz};
-  auto recon = [&](int d) -> int {
+  // lines of the x sweep: (t1 = y, t2 = z), t1 fastest; interior z planes = one contiguous range
+  const long long w0 = ny + 4, nl0 = w0 * (nz + 4);
+  auto recon_launch = [&](int d, long long lbeg, long long lcnt, long long gap_at, long long gap) {
     T* ff = (T*)c->FF[d & 1];
+    const int blocks = (int)((5 * lcnt + 127) / 128);
+    const LineRange lr{lbeg, lcnt, gap_at, gap};
+    if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    if (d == 1) recon_kernel<T, 1><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    c->total_launches += 1;
+  };
+  auto recon = [&](int d) -> int {
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
+    const long long nl = (long long)(n1 + 4) * (n2 + 4);
     prof_begin(c, HGKS_K_RECON, c->s2);
-    if (d == 0) recon_kernel<T, 0><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
-    if (d == 1) recon_kernel<T, 1><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
-    if (d == 2) recon_kernel<T, 2><<<recon_blocks(n1, n2), 128, 0, c->s2>>>(q, ff, g, c->ctl);
+    if (d == 0) {
+      recon_launch(0, 2 * w0, (long long)nz * w0, nl0, 0);                 // interior z planes
+      prof_end(c, HGKS_K_RECON, c->s2);
+      CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_halo, 0));
+      prof_begin(c, HGKS_K_RECON, c->s2);
+      recon_launch(0, 0, 4 * w0, 2 * w0, (long long)nz * w0);              // the 4 ghost planes
+    } else {
+      recon_launch(d, 0, nl, nl, 0);
+    }
     prof_end(c, HGKS_K_RECON, c->s2);
     CUDA_TRY(c, cudaEventRecord(c->ev_rec[d], c->s2));
     return HGKS_OK;
@@ -298,7 +495,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   if ((rc = recon(0)) || (rc = recon(1)) || (rc = flux(0))) return rc;
   CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_flux[0], 0));  // FF[0] free again
   if ((rc = recon(2)) || (rc = flux(1)) || (rc = flux(2))) return rc;
-  c->total_launches += 6;
+  c->total_launches += 3;
   CUDA_TRY(c, cudaGetLastError());
   return HGKS_OK;
 }
@@ -321,14 +518,14 @@ static int diagnostics_t(hgks_ctx* c) {
   // kernels; hgks_step resets it on entry anyway)
   CUDA_TRY(c, cudaMemsetAsync(&c->ctl->halt, 0, sizeof(int), c->s));
   int rc;
-  if ((rc = fill_ghosts<T>(c, Q))) return rc;
+  if ((rc = fill_ghosts<T>(c, Q, true))) return rc;
   const DiagGeo dg = diag_geo(c);
   double* out = c->diag_dev + DIAG_BLOCKS * NDIAG;
   diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->diag_dev);
   diag_final_kernel<NDIAG><<<1, DIAG_TPB, 0, c->s>>>(c->diag_dev, DIAG_BLOCKS, out);
   c->total_launches += 2;
   CUDA_TRY(c, cudaGetLastError());
-  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(out, out, NDIAG, ncclFloat64, ncclSum, c->comm, c->s));
+  if ((rc = coll_allreduce(c, out, NDIAG, 1))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(c->diag_host, out, NDIAG * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   CUDA_TRY(c, cudaStreamSynchronize(c->s));
   return HGKS_OK;
@@ -352,14 +549,14 @@ static int run_steps(hgks_ctx* c, int nsteps) {
     prof_end(c, HGKS_K_DT);
     c->total_launches += 1;
     // stage 1 at Q^n
-    if ((rc = fill_ghosts<T>(c, Qn))) return rc;
+    if ((rc = fill_ghosts<T>(c, Qn, false))) return rc;
     if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
     update_kernel<T, 1><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
                                                    c->ctl, c->bulk_dev);
     prof_end(c, HGKS_K_UPDATE);
     // stage 2 at Q* (same dt and windows, O-11)
-    if ((rc = fill_ghosts<T>(c, Qs))) return rc;
+    if ((rc = fill_ghosts<T>(c, Qs, false))) return rc;
     if ((rc = flux_sweeps<T, 2>(c, Qs))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
     update_kernel<T, 2><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
@@ -371,10 +568,9 @@ static int run_steps(hgks_ctx* c, int nsteps) {
       c->total_launches += 1;
     }
     CUDA_TRY(c, cudaGetLastError());
-    if (c->p.nranks > 1) {  // global max wave speed + global error flag
-      NCCL_TRY(c, ncclAllReduce(&c->ctl->red[0], &c->ctl->red[0], 2, ncclUint64, ncclMax, c->comm, c->s));
-      if (bulk) NCCL_TRY(c, ncclAllReduce(&c->ctl->bulk_new[0], &c->ctl->bulk_new[0], 2, ncclFloat64, ncclSum, c->comm, c->s));
-    }
+    // global max wave speed + global error flag; bulk sums of the force controller
+    if ((rc = coll_allreduce(c, &c->ctl->red[0], 2, 0))) return rc;
+    if (bulk && (rc = coll_allreduce(c, &c->ctl->bulk_new[0], 2, 1))) return rc;
     c->cur ^= 1;
   }
   commit_kernel<<<1, 32, 0, c->s>>>(c->ctl);
@@ -447,7 +643,10 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   if (p->force_mode != HGKS_FORCE_NONE && p->force_mode != HGKS_FORCE_CONST && p->force_mode != HGKS_FORCE_BULK)
     return fail(nullptr, HGKS_EINVAL, "bad force_mode");
   if (p->force_mode != HGKS_FORCE_NONE && !std::isfinite(p->force)) return fail(nullptr, HGKS_EINVAL, "force not finite");
-  if (p->nranks > 1 && !p->nccl_id) return fail(nullptr, HGKS_EINVAL, "nranks > 1 needs nccl_id");
+  if (p->nranks > 1 && !p->nccl_id && p->group_key == 0)
+    return fail(nullptr, HGKS_EINVAL, "nranks > 1 needs nccl_id or a loopback group_key");
+  if (p->nccl_id && p->group_key != 0) return fail(nullptr, HGKS_EINVAL, "nccl_id and group_key are exclusive");
+  if (p->group_key != 0 && p->nranks > LB_MAX) return fail(nullptr, HGKS_EINVAL, "loopback group: nranks > %d", LB_MAX);
   if (p->n[2] / p->nranks < 3) return fail(nullptr, HGKS_EINVAL, "nz/nranks < 3");
 
   hgks_ctx* c = new hgks_ctx();
@@ -503,7 +702,15 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   }
   for (int b = 0; b < 2; ++b) ok = ok && cudaMalloc(&c->FF[b], c->ff_elems * c->esz) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess;
+  {
+    int lo_pri = 0, hi_pri = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    ok = ok && cudaStreamCreateWithPriority(&c->sc, cudaStreamNonBlocking, hi_pri) == cudaSuccess;
+  }
   ok = ok && cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess;
+  for (cudaEvent_t* e : {&c->ev_xy, &c->ev_halo, &c->lb_post, &c->lb_done, &c->lb_rpost, &c->lb_rdone})
+    ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->red_tmp, ((size_t)c->n[1] * NSTAT + NDIAG + 16) * 8) == cudaSuccess;  // largest allreduce
   for (int d = 0; d < 3; ++d) {
     ok = ok && cudaEventCreateWithFlags(&c->ev_rec[d], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_flux[d], cudaEventDisableTiming) == cudaSuccess;
@@ -569,7 +776,10 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     fail(c, HGKS_ECUDA, "initialisation copy failed");
     return bail(HGKS_ECUDA);
   }
-  if (p->nranks > 1) {
+  if (p->nranks > 1 && p->group_key != 0) {
+    int rc = lb_join(c);
+    if (rc) return bail(rc);
+  } else if (p->nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, p->nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, p->nranks, id, p->rank);
@@ -620,8 +830,7 @@ static int set_state_t(hgks_ctx* c) {
   cfl_kernel<T><<<blocks_for(ncell, 256), 256, 0, c->s>>>(Q, g, c->p.gamma, c->ctl);
   c->total_launches += 2;
   CUDA_TRY(c, cudaGetLastError());
-  if (c->p.nranks > 1)
-    NCCL_TRY(c, ncclAllReduce(&c->ctl->red[0], &c->ctl->red[0], 2, ncclUint64, ncclMax, c->comm, c->s));
+  if ((rc = coll_allreduce(c, &c->ctl->red[0], 2, 0))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
   CUDA_TRY(c, cudaStreamSynchronize(c->s));
   if (h->red[1]) {
@@ -735,7 +944,8 @@ static int plane_stats_t(hgks_ctx* c, double* out) {
   c->total_launches += 1;
   CUDA_TRY(c, cudaGetLastError());
   const size_t cnt = (size_t)c->n[1] * NSTAT;
-  if (c->p.nranks > 1) NCCL_TRY(c, ncclAllReduce(c->stats_dev, c->stats_dev, cnt, ncclFloat64, ncclSum, c->comm, c->s));
+  int rc;
+  if ((rc = coll_allreduce(c, c->stats_dev, cnt, 1))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(out, c->stats_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->s));
   CUDA_TRY(c, cudaStreamSynchronize(c->s));
   const double inv = 1.0 / ((double)c->n[0] * c->n[2]);
@@ -771,7 +981,13 @@ int hgks_destroy(hgks_ctx* c) {
   if (!c) return HGKS_OK;
   cudaSetDevice(c->dev);
   if (c->s) cudaStreamSynchronize(c->s);
+  if (c->sc) cudaStreamSynchronize(c->sc);
   if (c->comm) ncclCommDestroy(c->comm);
+  lb_leave(c);
+  cudaFree(c->red_tmp);
+  if (c->sc) cudaStreamDestroy(c->sc);
+  for (cudaEvent_t e : {c->ev_xy, c->ev_halo, c->lb_post, c->lb_done, c->lb_rpost, c->lb_rdone})
+    if (e) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) cudaFree(c->Q[b]);
   cudaFree(c->Qs);
   for (int d = 0; d < 3; ++d) cudaFree(c->F[d]);
@@ -873,7 +1089,7 @@ static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
   h->halt = 0;
   CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
   int rc;
-  if ((rc = fill_ghosts<T>(c, Q))) return rc;
+  if ((rc = fill_ghosts<T>(c, Q, false))) return rc;
   if ((rc = flux_sweeps<T, 1>(c, Q))) return rc;
   const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   double *dL_ = nullptr, *dDL = nullptr;

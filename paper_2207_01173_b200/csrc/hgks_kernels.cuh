@@ -145,18 +145,25 @@ __device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
   return L;
 }
 
+// Subset of the face lines of one sweep: lines lbeg + j for j in [0, lcnt), where j >= gap_at
+// skips ahead by gap (two disjoint ranges in one launch: the ghost-plane lines of the x sweep).
+struct LineRange {
+  long long lbeg, lcnt, gap_at, gap;
+};
+
 // One thread per (line, component): marches along the normal with a 6-cell register ring, so
 // every cell's WENO edge pair is computed exactly once.
 template <typename T, int DIR>
 __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
-                                                    const Ctl* __restrict__ ctl) {
+                                                    const Ctl* __restrict__ ctl, LineRange lr) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;
   const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= 5 * L.nl) return;
-  const int c = (int)(e / L.nl);
-  const long long l = e % L.nl;
+  if (e >= 5 * lr.lcnt) return;
+  const int c = (int)(e / lr.lcnt);
+  const long long j = e % lr.lcnt;
+  const long long l = lr.lbeg + j + (j >= lr.gap_at ? lr.gap : 0);
   int t1, t2;
   if (DIR == 1) {
     t1 = (int)(l / (L.n2 + 4)) - 2;

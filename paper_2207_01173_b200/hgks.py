@@ -48,7 +48,8 @@ class Params(C.Structure):
                 ("omega", C.c_double), ("T_wall", C.c_double), ("cfl", C.c_double), ("dt_fixed", C.c_double),
                 ("precision", C.c_int), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("device", C.c_int32), ("nccl_id", C.c_void_p), ("stream", C.c_void_p),
-                ("force_mode", C.c_int), ("force", C.c_double), ("force_target", C.c_double)]
+                ("force_mode", C.c_int), ("force", C.c_double), ("force_target", C.c_double),
+                ("group_key", C.c_int64)]
 
 
 class HaloPlan(C.Structure):
@@ -127,7 +128,7 @@ def make_params(n, lo, hi, gamma=1.4, mu=0.0, prandtl=1.0, mu_law=HGKS_MU_CONST,
                 omega=0.0, cfl=0.4, dt_fixed=0.0, precision=HGKS_FP64, rank=0, nranks=1,
                 device=0, nccl_id=None, stream=None, bc=(HGKS_PERIODIC,) * 3,
                 stretch=(HGKS_UNIFORM,) * 3, stretch_b=(0.0, 0.0, 0.0), T_wall=1.0,
-                force_mode=HGKS_FORCE_NONE, force=0.0, force_target=0.0):
+                force_mode=HGKS_FORCE_NONE, force=0.0, force_target=0.0, group_key=0):
     p = Params()
     for d in range(3):
         p.n[d] = int(n[d])
@@ -144,6 +145,7 @@ def make_params(n, lo, hi, gamma=1.4, mu=0.0, prandtl=1.0, mu_law=HGKS_MU_CONST,
     p.nccl_id = C.cast(p._id_buf, C.c_void_p) if nccl_id is not None else None
     p.stream = stream
     p.force_mode, p.force, p.force_target = int(force_mode), float(force), float(force_target)
+    p.group_key = int(group_key)
     return p
 
 
@@ -249,6 +251,38 @@ def hgks_test_face_flux(ctx, d: int, n) -> np.ndarray:
     out = np.zeros((10, *dims))
     _check(lib().hgks_test_face_flux(ctx, d, out.ctypes.data_as(_dp)), ctx)
     return out
+
+
+def run_loopback_group(nranks: int, fn, key: int | None = None):
+    """Run fn(rank, nranks, group_key) on nranks host threads (one loopback-group rank each; every
+    rank's hgks_* calls must come from its own thread, ctypes releases the GIL).  Returns the list
+    of results by rank; re-raises the first exception."""
+    import threading
+    key = key if key is not None else next(_group_keys)
+    out, err = [None] * nranks, []
+
+    def work(r):
+        try:
+            out[r] = fn(r, nranks, key)
+        except BaseException as e:  # noqa: BLE001 (propagated below)
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
+def _keys():
+    import itertools
+    return itertools.count(os.getpid() * 1000 + 1)
+
+
+_group_keys = _keys()
 
 
 class Solver:
