@@ -341,7 +341,8 @@ def main():
     if "fp32" in results:
         r32 = results["fp32"]
         line["fp32"] = {"value": r32["value"], "ms_per_step": r32["ms_per_step"], "clocks": r32["clocks"],
-                        "e2e": r32.get("e2e"), "speedup_vs_fp64": r32["value"] / r64["value"]}
+                        "e2e": r32.get("e2e"), "speedup_vs_fp64": r32["value"] / r64["value"],
+                        "kernel_ms_per_step": {k: v / args.steps for k, v in r32["ms_k"].items()}}
     if not args.no_cpu and not channel:
         v, cores, sec, sample = cpu_baseline(n, args.cpu_planes, prm["mu"], (2 * math.pi / n,) * 3)
         line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",

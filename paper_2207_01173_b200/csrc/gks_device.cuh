@@ -289,6 +289,13 @@ struct GpFlux {
   T rr, irr, Ur, Vr, Wr, thr, hr0, hr1;
   T r0, ir0, U0, V0, W0, th0;
   T h, idt, dt, prf, ik3;
+#ifndef HGKS_GSHARE
+#define HGKS_GSHARE 1
+#endif
+  // HGKS_GSHARE: the shared factors of the Gamma / Gamma' coefficients, computed once in begin()
+  //   tc13 = tau (1-h)(3-h)/dt, ttc13 = tau tc13, hb = tau h (2-h), gp1 = 4 tau (1-h)^2/dt^2,
+  //   gp2 = 4 tau (1-h)(dt h - 2 tau (1-h))/dt^2, tgp1 = tau gp1
+  T tc13, ttc13, hb, gp1, gp2, tgp1;
   T F[5], dF[5], tau;
 
   HD void begin(const GasK<T>& g, const T (&WL)[5], const T (&WR)[5], T dt_, T idt_) {
@@ -339,6 +346,17 @@ struct GpFlux {
     // (below 1e-20 -- dt/tau > 92, e.g. every low-Mach TGV face -- h changes no Gamma above rounding)
     const T harg = -T(0.5) * dt * rcp(tau);
     h = (tau > T(0) && harg > T(-46)) ? m_exp(harg) : T(0);
+    if (HGKS_GSHARE) {
+      const T om = T(1) - h;
+      const T c13 = om * (T(3) - h) * idt;
+      const T idt2 = idt * idt;
+      tc13 = tau * c13;
+      ttc13 = tau * tc13;
+      hb = tau * h * (T(2) - h);
+      gp1 = T(4) * tau * om * om * idt2;
+      gp2 = T(4) * tau * om * (dt * h - T(2) * tau * om) * idt2;
+      tgp1 = tau * gp1;
+    }
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       F[k] = T(0);
@@ -348,6 +366,24 @@ struct GpFlux {
 
   // closed-form time coefficients: Gamma_1..3 (g0 terms) or Gamma_4..6 (g_l, g_r)
   HD void gammas(bool eq, T& ga, T& gb, T& gc, T& gpa, T& gpb, T& gpc) const {
+    if (HGKS_GSHARE) {
+      if (eq) {
+        ga = T(1) - tc13;
+        gb = -tau - hb + T(2) * ttc13;  // -tau (1 + 2h - h^2) + 2 tau^2 c13
+        gc = -tau + ttc13;
+        gpa = gp1;
+        gpb = gp2;
+        gpc = T(1) - tgp1;
+      } else {
+        ga = tc13;
+        gb = hb - T(2) * ttc13;
+        gc = -ttc13;
+        gpa = -gp1;
+        gpb = -gp2;
+        gpc = tgp1;
+      }
+      return;
+    }
     const T om = T(1) - h;
     const T c13 = om * (T(3) - h) * idt;
     const T tt = tau * tau;

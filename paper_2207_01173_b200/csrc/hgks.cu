@@ -446,7 +446,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_xy, 0));
   const int n3[3] = {nx, ny, nz};
   // lines of the x sweep: (t1 = y, t2 = z), t1 fastest; interior z planes = one contiguous range
-  const long long w0 = ny + 4, nl0 = w0 * (nz + 4);
+  const long long w0 = ff_pitch(ny, (int)sizeof(T)), nl0 = w0 * (nz + 4);
   auto recon_launch = [&](int d, long long lbeg, long long lcnt, long long gap_at, long long gap) {
     T* ff = (T*)c->FF[d & 1];
     const int blocks = (int)((5 * lcnt + 127) / 128);
@@ -458,7 +458,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   };
   auto recon = [&](int d) -> int {
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    const long long nl = (long long)(n1 + 4) * (n2 + 4);
+    const long long nl = d == 1 ? (long long)(n1 + 4) * (n2 + 4) : (long long)ff_pitch(n1, (int)sizeof(T)) * (n2 + 4);
     prof_begin(c, HGKS_K_RECON, c->s2);
     if (d == 0) {
       recon_launch(0, 2 * w0, (long long)nz * w0, nl0, 0);                 // interior z planes
@@ -697,10 +697,15 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   c->ff_elems = 0;
   for (int d = 0; d < 3; ++d) {
     const int n3[3] = {c->n[0], c->n[1], c->nzl};
-    const size_t e = 30ull * (n3[d] + 1) * (n3[(d + 1) % 3] + 4) * (n3[(d + 2) % 3] + 4);
+    const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
+    const size_t p1 = d == 1 ? (size_t)n1 + 4 : (size_t)ff_pitch(n1, (int)c->esz);
+    const size_t e = 30ull * (n3[d] + 1) * p1 * (n2 + 4) + 16;  // +16: slack for 16-byte copies
     if (e > c->ff_elems) c->ff_elems = e;
   }
-  for (int b = 0; b < 2; ++b) ok = ok && cudaMalloc(&c->FF[b], c->ff_elems * c->esz) == cudaSuccess;
+  for (int b = 0; b < 2; ++b) {
+    ok = ok && cudaMalloc(&c->FF[b], c->ff_elems * c->esz) == cudaSuccess;
+    ok = ok && cudaMemset(c->FF[b], 0, c->ff_elems * c->esz) == cudaSuccess;  // pad lines stay 0
+  }
   ok = ok && cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess;
   {
     int lo_pri = 0, hi_pri = 0;

@@ -115,6 +115,10 @@ constexpr size_t flux_smem_bytes() {
   return sizeof(T) * (6 * 5 * SA_C + TL2 * 5 * SB_RC);
 }
 
+#ifndef HGKS_CP16
+#define HGKS_CP16 1  // 16-byte face-field copies (fp64, DIR 0 / 2): +7 % fp64 step rate; no gain fp32
+#endif
+
 // ---- normal reconstruction (A2): face fields of every face-line of one direction -------------
 // Face-field array of direction DIR (elements of T): ff[field][comp][fn][line], fields
 //   0 Ql, 1 Qr, 2 dQl/dn, 3 dQr/dn, 4 C, 5 D   (normal_fields, O-3 / O-6)
@@ -122,12 +126,21 @@ constexpr size_t flux_smem_bytes() {
 // (t1, t2) in [-2, n_t1+2) x [-2, n_t2+2) (the +-2 halo the tangential stencils need), line index
 // with the x-most tangent fastest: DIR 0 (t1 = y, t2 = z) and DIR 2 (t1 = x, t2 = y): t1 fastest;
 // DIR 1 (t1 = z, t2 = x): t2 fastest.
+// Pitch of the fast tangential axis in the face-field line index of DIR 0 / 2: n_t1 + 4 lines
+// rounded up to 16 bytes, so a tile row of lines starts 16-byte aligned and the flux kernel's
+// copy moves 16-byte chunks (2 fp64 / 4 fp32 lines).  The pad lines are never written by the
+// reconstruction and only ever feed faces outside the domain.
+__host__ __device__ constexpr int ff_pitch(int n_fast, int esz) {
+  return (n_fast + 4 + (16 / esz) - 1) / (16 / esz) * (16 / esz);
+}
+
 template <typename T, int DIR>
 struct FFLayout {
   int n1, n2, nf;   // tangential cells, faces along the normal
-  long long nl;     // lines per face plane
+  int p;            // pitch of the fast axis (t1 for DIR 0/2, t2 for DIR 1)
+  long long nl;     // lines per face plane (including pad lines)
   __device__ __forceinline__ long long line(int t1, int t2) const {
-    return DIR == 1 ? (long long)(t1 + 2) * (n2 + 4) + (t2 + 2) : (long long)(t2 + 2) * (n1 + 4) + (t1 + 2);
+    return DIR == 1 ? (long long)(t1 + 2) * p + (t2 + 2) : (long long)(t2 + 2) * p + (t1 + 2);
   }
   __device__ __forceinline__ long long at(int f, int c, int fn, long long l) const {
     return ((long long)(f * 5 + c) * nf + fn) * nl + l;
@@ -141,7 +154,8 @@ __device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
   L.n1 = g.n[A1];
   L.n2 = g.n[A2];
   L.nf = g.n[DIR] + 1;
-  L.nl = (long long)(L.n1 + 4) * (L.n2 + 4);
+  L.p = DIR == 1 ? L.n2 + 4 : ff_pitch(L.n1, (int)sizeof(T));
+  L.nl = (long long)L.p * (DIR == 1 ? L.n1 + 4 : L.n2 + 4);
   return L;
 }
 
@@ -166,11 +180,12 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const long long l = lr.lbeg + j + (j >= lr.gap_at ? lr.gap : 0);
   int t1, t2;
   if (DIR == 1) {
-    t1 = (int)(l / (L.n2 + 4)) - 2;
-    t2 = (int)(l % (L.n2 + 4)) - 2;
+    t1 = (int)(l / L.p) - 2;
+    t2 = (int)(l % L.p) - 2;
   } else {
-    t2 = (int)(l / (L.n1 + 4)) - 2;
-    t1 = (int)(l % (L.n1 + 4)) - 2;
+    t2 = (int)(l / L.p) - 2;
+    t1 = (int)(l % L.p) - 2;
+    if (t1 >= L.n1 + 2) return;  // pad line
   }
   const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
   const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
@@ -233,31 +248,58 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
     const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sA);
-    constexpr int NLINE = TL1 * TL2;
-    constexpr int NPASS = (NLINE + NTHREADS_FLUX - 1) / NTHREADS_FLUX;
+    const T* fbase = ff + (long long)fn * L.nl;
+    constexpr int VEC = 16 / (int)sizeof(T);  // lines per 16-byte chunk
+    constexpr int NCH = TL1 / VEC;            // chunks per tile row
+    // DIR 0 / 2: t1 is the contiguous axis of the array and every tile row of TL1 lines starts
+    // 16-byte aligned (ff_pitch, t10 % 8 == 0): 16-byte copies.  DIR 1, and tiles whose rows would
+    // run past line n1+1 (ragged edge), copy single lines, clamped.
+    if (HGKS_CP16 && sizeof(T) == 8 && DIR != 1 && t10 + TL1 - 2 <= n1 + 2) {
+      // item = (chunk, row l2, fc group): FS groups of 30/FS (field, component) planes each
+      constexpr int NRC = TL2 * NCH;
+      constexpr int FS = (NTHREADS_FLUX / NRC) >= 6 ? 6 : ((NTHREADS_FLUX / NRC) >= 5 ? 5 : ((NTHREADS_FLUX / NRC) >= 3 ? 3 : 1));
+      constexpr int FPG = 30 / FS;
+      static_assert(30 % FS == 0, "fc groups");
+      const int j = threadIdx.x;
+      if (j < NRC * FS) {
+        const int ch = j % NCH, l2 = (j / NCH) % TL2, fg = j / NRC;
+        const int t2 = min(t20 + l2 - 2, n2 + 1);
+        const T* src = fbase + (long long)(fg * FPG) * fstride + L.line(t10 - 2 + ch * VEC, t2);
+        unsigned dst = sbase + (unsigned)(((fg * FPG) * SA_C + l2 * TL1 + ch * VEC) * (int)sizeof(T));
 #pragma unroll
-    for (int pass = 0; pass < NPASS; ++pass) {
-      const int j = threadIdx.x + pass * NTHREADS_FLUX;
-      if (j < NLINE) {
-        int l1, l2;
-        if (DIR == 1) {  // t2 is the contiguous axis of the array
-          l2 = j % TL2;
-          l1 = j / TL2;
-        } else {
-          l1 = j % TL1;
-          l2 = j / TL1;
-        }
-        const int t1 = min(t10 + l1 - 2, n1 + 1), t2 = min(t20 + l2 - 2, n2 + 1);  // ragged tiles: clamp
-        const T* src = ff + (long long)fn * L.nl + L.line(t1, t2);
-        unsigned dst = sbase + (unsigned)((l2 * TL1 + l1) * sizeof(T));
-#pragma unroll
-        for (int fc = 0; fc < 30; ++fc) {
-          if (sizeof(T) == 8)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-          else
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+        for (int f = 0; f < FPG; ++f) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
           src += fstride;
           dst += SA_C * sizeof(T);
+        }
+      }
+    } else {
+      constexpr int NLINE = TL1 * TL2;
+      constexpr int NPASS = (NLINE + NTHREADS_FLUX - 1) / NTHREADS_FLUX;
+#pragma unroll
+      for (int pass = 0; pass < NPASS; ++pass) {
+        const int j = threadIdx.x + pass * NTHREADS_FLUX;
+        if (j < NLINE) {
+          int l1, l2;
+          if (DIR == 1) {  // t2 is the contiguous axis of the array
+            l2 = j % TL2;
+            l1 = j / TL2;
+          } else {
+            l1 = j % TL1;
+            l2 = j / TL1;
+          }
+          const int t1 = min(t10 + l1 - 2, n1 + 1), t2 = min(t20 + l2 - 2, n2 + 1);  // ragged tiles: clamp
+          const T* src = fbase + L.line(t1, t2);
+          unsigned dst = sbase + (unsigned)((l2 * TL1 + l1) * sizeof(T));
+#pragma unroll
+          for (int fc = 0; fc < 30; ++fc) {
+            if (sizeof(T) == 8)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+            src += fstride;
+            dst += SA_C * sizeof(T);
+          }
         }
       }
     }

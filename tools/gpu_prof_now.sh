@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+TAG=${1:-cur}
+timeout 300 python tools/phase_timing.py 128 > gpurun_out/phase_$TAG.log 2>&1; echo phase rc=$?; cat gpurun_out/phase_$TAG.log | tail -2
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flux_kernel -s 3 -c 2 -o gpurun_out/prof_$TAG python bench.py --n 128 --steps 1 --warmup 1 --no-fp32 --no-e2e --no-cpu > gpurun_out/ncu_$TAG.log 2>&1; echo ncu rc=$?
+cp paper_2207_01173_b200/libhgks.so gpurun_out/libhgks_$TAG.so
