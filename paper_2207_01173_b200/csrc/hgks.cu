@@ -452,13 +452,12 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     const int blocks = (int)((5 * lcnt + 127) / 128);
     const LineRange lr{lbeg, lcnt, gap_at, gap};
     if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
-    if (d == 1) recon_kernel<T, 1><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
     if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
     c->total_launches += 1;
   };
   auto recon = [&](int d) -> int {
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    const long long nl = d == 1 ? (long long)(n1 + 4) * (n2 + 4) : (long long)ff_pitch(n1, (int)sizeof(T)) * (n2 + 4);
+    const long long nl = (long long)ff_pitch(n1, (int)sizeof(T)) * (n2 + 4);
     prof_begin(c, HGKS_K_RECON, c->s2);
     if (d == 0) {
       recon_launch(0, 2 * w0, (long long)nz * w0, nl0, 0);                 // interior z planes
@@ -466,6 +465,10 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
       CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_halo, 0));
       prof_begin(c, HGKS_K_RECON, c->s2);
       recon_launch(0, 0, 4 * w0, 2 * w0, (long long)nz * w0);              // the 4 ghost planes
+    } else if (d == 1) {  // y sweep: z-fastest face-field lines
+      dim3 grid((nz + 4 + RZ_Z - 1) / RZ_Z, (nx + 4 + RZ_X - 1) / RZ_X, 5);
+      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, (T*)c->FF[1], g, c->ctl);
+      c->total_launches += 1;
     } else {
       recon_launch(d, 0, nl, nl, 0);
     }
@@ -698,7 +701,7 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   for (int d = 0; d < 3; ++d) {
     const int n3[3] = {c->n[0], c->n[1], c->nzl};
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    const size_t p1 = d == 1 ? (size_t)n1 + 4 : (size_t)ff_pitch(n1, (int)c->esz);
+    const size_t p1 = (size_t)ff_pitch(n1, (int)c->esz);
     const size_t e = 30ull * (n3[d] + 1) * p1 * (n2 + 4) + 16;  // +16: slack for 16-byte copies
     if (e > c->ff_elems) c->ff_elems = e;
   }

@@ -116,7 +116,7 @@ constexpr size_t flux_smem_bytes() {
 }
 
 #ifndef HGKS_CP16
-#define HGKS_CP16 1  // 16-byte face-field copies (fp64, DIR 0 / 2): +7 % fp64 step rate; no gain fp32
+#define HGKS_CP16 1  // 16-byte face-field copies (fp64): +7 % fp64 step rate (x, z sweeps); no gain fp32
 #endif
 
 // ---- normal reconstruction (A2): face fields of every face-line of one direction -------------
@@ -126,22 +126,21 @@ constexpr size_t flux_smem_bytes() {
 // (t1, t2) in [-2, n_t1+2) x [-2, n_t2+2) (the +-2 halo the tangential stencils need), line index
 // with the x-most tangent fastest: DIR 0 (t1 = y, t2 = z) and DIR 2 (t1 = x, t2 = y): t1 fastest;
 // DIR 1 (t1 = z, t2 = x): t2 fastest.
-// Pitch of the fast tangential axis in the face-field line index of DIR 0 / 2: n_t1 + 4 lines
-// rounded up to 16 bytes, so a tile row of lines starts 16-byte aligned and the flux kernel's
-// copy moves 16-byte chunks (2 fp64 / 4 fp32 lines).  The pad lines are never written by the
-// reconstruction and only ever feed faces outside the domain.
-__host__ __device__ constexpr int ff_pitch(int n_fast, int esz) {
-  return (n_fast + 4 + (16 / esz) - 1) / (16 / esz) * (16 / esz);
+// Pitch of the t1 axis in the face-field line index: n_t1 + 4 lines rounded up to 16 bytes, so a
+// tile row of lines starts 16-byte aligned and the flux kernel's copy moves 16-byte chunks (2 fp64
+// / 4 fp32 lines).  The pad lines are never written by the reconstruction and only ever feed
+// faces outside the domain.
+__host__ __device__ constexpr int ff_pitch(int n_t1, int esz) {
+  return (n_t1 + 4 + (16 / esz) - 1) / (16 / esz) * (16 / esz);
 }
 
+// line index of tangential line (t1, t2), t1 fastest, for every direction
 template <typename T, int DIR>
 struct FFLayout {
   int n1, n2, nf;   // tangential cells, faces along the normal
-  int p;            // pitch of the fast axis (t1 for DIR 0/2, t2 for DIR 1)
+  int p;            // pitch of t1
   long long nl;     // lines per face plane (including pad lines)
-  __device__ __forceinline__ long long line(int t1, int t2) const {
-    return DIR == 1 ? (long long)(t1 + 2) * p + (t2 + 2) : (long long)(t2 + 2) * p + (t1 + 2);
-  }
+  __device__ __forceinline__ long long line(int t1, int t2) const { return (long long)(t2 + 2) * p + (t1 + 2); }
   __device__ __forceinline__ long long at(int f, int c, int fn, long long l) const {
     return ((long long)(f * 5 + c) * nf + fn) * nl + l;
   }
@@ -154,8 +153,8 @@ __device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
   L.n1 = g.n[A1];
   L.n2 = g.n[A2];
   L.nf = g.n[DIR] + 1;
-  L.p = DIR == 1 ? L.n2 + 4 : ff_pitch(L.n1, (int)sizeof(T));
-  L.nl = (long long)L.p * (DIR == 1 ? L.n1 + 4 : L.n2 + 4);
+  L.p = ff_pitch(L.n1, (int)sizeof(T));
+  L.nl = (long long)L.p * (L.n2 + 4);
   return L;
 }
 
@@ -166,7 +165,8 @@ struct LineRange {
 };
 
 // One thread per (line, component): marches along the normal with a 6-cell register ring, so
-// every cell's WENO edge pair is computed exactly once.
+// every cell's WENO edge pair is computed exactly once.  x and z sweeps (t1 = y / x is also the
+// fastest axis of the state, so reads and writes are coalesced); the y sweep is recon_yz_kernel.
 template <typename T, int DIR>
 __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
                                                     const Ctl* __restrict__ ctl, LineRange lr) {
@@ -178,15 +178,9 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const int c = (int)(e / lr.lcnt);
   const long long j = e % lr.lcnt;
   const long long l = lr.lbeg + j + (j >= lr.gap_at ? lr.gap : 0);
-  int t1, t2;
-  if (DIR == 1) {
-    t1 = (int)(l / L.p) - 2;
-    t2 = (int)(l % L.p) - 2;
-  } else {
-    t2 = (int)(l / L.p) - 2;
-    t1 = (int)(l % L.p) - 2;
-    if (t1 >= L.n1 + 2) return;  // pad line
-  }
+  static_assert(DIR != 1, "the y sweep is recon_yz_kernel");
+  const int t2 = (int)(l / L.p) - 2, t1 = (int)(l % L.p) - 2;
+  if (t1 >= L.n1 + 2) return;  // pad line
   const long long sN = (DIR == 0) ? 1 : (DIR == 1 ? g.px : g.plane);
   const long long s1 = (A1 == 0) ? 1 : (A1 == 1 ? g.px : g.plane);
   const long long s2 = (A2 == 0) ? 1 : (A2 == 1 ? g.px : g.plane);
@@ -205,6 +199,52 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
     if (fn >= 0) {
       const T ih = jfn[fn];  // metric of the face (O-18; 1/h on uniform axes)
+      ff[L.at(0, c, fn, l)] = Bp;
+      ff[L.at(1, c, fn, l)] = Ac;
+      ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
+      ff[L.at(3, c, fn, l)] = (T(-4) * Ac - T(2) * Bc + T(6) * s3) * ih;
+      ff[L.at(4, c, fn, l)] = (-s1v + T(7) * s2v + T(7) * s3 - s4) * T(1.0 / 12.0);
+      ff[L.at(5, c, fn, l)] = (s1v - T(15) * s2v + T(15) * s3 - s4) * (T(1.0 / 12.0) * ih);
+    }
+    s1v = s2v;
+    s2v = s3;
+    s3 = s4;
+    s4 = s5;
+    Ap = Ac;
+    Bp = Bc;
+  }
+}
+
+// y sweep (normal y, t1 = z, t2 = x).  The face-field lines are t1-fastest in every direction (so
+// the flux kernel copies 16-byte chunks), here z-fastest while the state is x-fastest: lanes run
+// along z (stores coalesced) and the 4 warps of a block take 4 consecutive x, so the strided state
+// reads of one warp share their 32-byte sectors with the other three warps (served from L1).
+// Measured against a shared-memory transpose (32 x by 8/16/24 z per block): the transpose blocks
+// hold shared memory and barriers, and slow the concurrent x-sweep flux kernel more than they gain.
+constexpr int RZ_Z = 32, RZ_X = 4;
+template <typename T>
+__global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
+                                                                const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  const FFLayout<T, 1> L = ff_layout<T, 1>(g);
+  const int tz = threadIdx.x % RZ_Z, tx = threadIdx.x / RZ_Z;
+  const int c = blockIdx.z;
+  const int z = blockIdx.x * RZ_Z + tz - 2, x = blockIdx.y * RZ_X + tx - 2;
+  if (z >= g.n[2] + 2 || x >= g.n[0] + 2) return;
+  const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 2 : (c == 2 ? 3 : 1)));  // (V, W, U) frame (O-23)
+  const long long sN = g.px;
+  const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + (long long)z * g.plane + x;
+  const T* jfn = g.jf[1];
+  const long long l = L.line(z, x);
+  T s1v = p[0], s2v = p[sN], s3 = p[2 * sN], s4 = p[3 * sN], s5;
+  T Ap = T(0), Bp = T(0);
+  const int nf = L.nf;
+  for (int fn = -1; fn < nf; ++fn) {
+    s5 = p[(fn + 5) * sN];
+    T Ac, Bc;
+    weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);
+    if (fn >= 0) {
+      const T ih = jfn[fn];
       ff[L.at(0, c, fn, l)] = Bp;
       ff[L.at(1, c, fn, l)] = Ac;
       ff[L.at(2, c, fn, l)] = (T(2) * Ap + T(4) * Bp - T(6) * s2v) * ih;
@@ -251,10 +291,10 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
     const T* fbase = ff + (long long)fn * L.nl;
     constexpr int VEC = 16 / (int)sizeof(T);  // lines per 16-byte chunk
     constexpr int NCH = TL1 / VEC;            // chunks per tile row
-    // DIR 0 / 2: t1 is the contiguous axis of the array and every tile row of TL1 lines starts
-    // 16-byte aligned (ff_pitch, t10 % 8 == 0): 16-byte copies.  DIR 1, and tiles whose rows would
-    // run past line n1+1 (ragged edge), copy single lines, clamped.
-    if (HGKS_CP16 && sizeof(T) == 8 && DIR != 1 && t10 + TL1 - 2 <= n1 + 2) {
+    // t1 is the contiguous axis of the array and every tile row of TL1 lines starts 16-byte aligned
+    // (ff_pitch, t10 % 8 == 0): 16-byte copies.  Tiles whose rows would run past line n1+1 (ragged
+    // edge) copy single lines, clamped.
+    if (HGKS_CP16 && sizeof(T) == 8 && t10 + TL1 - 2 <= n1 + 2) {
       // item = (chunk, row l2, fc group): FS groups of 30/FS (field, component) planes each
       constexpr int NRC = TL2 * NCH;
       constexpr int FS = (NTHREADS_FLUX / NRC) >= 6 ? 6 : ((NTHREADS_FLUX / NRC) >= 5 ? 5 : ((NTHREADS_FLUX / NRC) >= 3 ? 3 : 1));
@@ -280,14 +320,7 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
       for (int pass = 0; pass < NPASS; ++pass) {
         const int j = threadIdx.x + pass * NTHREADS_FLUX;
         if (j < NLINE) {
-          int l1, l2;
-          if (DIR == 1) {  // t2 is the contiguous axis of the array
-            l2 = j % TL2;
-            l1 = j / TL2;
-          } else {
-            l1 = j % TL1;
-            l2 = j / TL1;
-          }
+          const int l1 = j % TL1, l2 = j / TL1;
           const int t1 = min(t10 + l1 - 2, n1 + 1), t2 = min(t20 + l2 - 2, n2 + 1);  // ragged tiles: clamp
           const T* src = fbase + L.line(t1, t2);
           unsigned dst = sbase + (unsigned)((l2 * TL1 + l1) * sizeof(T));
