@@ -479,16 +479,21 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   auto flux = [&](int d) -> int {
     T* ff = (T*)c->FF[d & 1];
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, (n3[d] + 1 + HGKS_FLUX_TPB - 1) / HGKS_FLUX_TPB);
+    // faces per block along the normal: HGKS_FLUX_TPB (measured best at 256^3: 16 > 8 > 4 > 2), halved
+    // while the grid would have fewer than 8 blocks per SM
+    const long long tiles = (long long)((n1 + TT1 - 1) / TT1) * ((n2 + TT2 - 1) / TT2);
+    int fpb = HGKS_FLUX_TPB;
+    while (fpb > 2 && tiles * ((n3[d] + 1 + fpb - 1) / fpb) < 148LL * 8) fpb /= 2;
+    dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, (n3[d] + 1 + fpb - 1) / fpb);
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
     const bool prf = c->p.prandtl != 1.0;
-    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
-    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
-    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
-    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl);
-    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl);
-    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl);
+    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
+    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
+    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
+    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
+    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
+    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
     prof_end(c, HGKS_K_FLUX_X + d);
     CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
     return HGKS_OK;

@@ -93,7 +93,7 @@ __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, 
 }
 
 #ifndef HGKS_FLUX_TPB
-#define HGKS_FLUX_TPB 2  // consecutive normal faces per flux block (face-field prefetch depth)
+#define HGKS_FLUX_TPB 16  // max consecutive normal faces per flux block (host lowers it for small grids)
 #endif
 #ifndef HGKS_FLUX_MINB
 #define HGKS_FLUX_MINB 2  // resident flux blocks per SM (register budget 128/thread)
@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
 // warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
 template <typename T, int DIR, int STAGE, bool PRF>
 __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
-    flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl) {
+    flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl,
+                int fpb) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -280,10 +281,10 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
 
   const int n1 = g.n[A1], n2 = g.n[A2];
   const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2;
-  // HGKS_FLUX_TPB consecutive normal faces per block: the face fields of face fn+1 are copied
+  // fpb consecutive normal faces per block: the face fields of face fn+1 are copied
   // (cp.async) into sA while face fn is in phase C, so only the first copy's latency is exposed
-  const int fn0 = blockIdx.z * HGKS_FLUX_TPB;
-  const int nfn = min(HGKS_FLUX_TPB, g.n[DIR] + 1 - fn0);
+  const int fn0 = blockIdx.z * fpb;
+  const int nfn = min(fpb, g.n[DIR] + 1 - fn0);
   auto issue_A = [&](int fn) {
     const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
     const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
