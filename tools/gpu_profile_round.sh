@@ -10,6 +10,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 python bench.py --workload channel --no-cpu > gpurun_out/bench_channel_$TAG.json 2> gpurun_out/bench_channel_$TAG.err; echo channel rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-launch rc=$?
 M=gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_ffma_pred_on.sum,smsp__sass_thread_inst_executed_op_fmul_pred_on.sum,smsp__sass_thread_inst_executed_op_fadd_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active
-timeout 900 ncu --metrics $M --clock-control none -k regex:"flux_kernel|recon_kernel|update_kernel" -c 16 --csv --log-file gpurun_out/counters64_$TAG.csv python bench.py --steps 1 --warmup 1 --no-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-c64 rc=$?
-timeout 900 ncu --metrics $M --clock-control none -k regex:"flux_kernel|recon_kernel|update_kernel" -c 16 --csv --log-file gpurun_out/counters32_$TAG.csv python bench.py --steps 1 --warmup 1 --only-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-c32 rc=$?
+timeout 900 ncu --metrics $M --clock-control none -k regex:"flux_kernel|recon_|update_kernel" -c 16 --csv --log-file gpurun_out/counters64_$TAG.csv python bench.py --steps 1 --warmup 1 --no-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-c64 rc=$?
+timeout 900 ncu --metrics $M --clock-control none -k regex:"flux_kernel|recon_|update_kernel" -c 16 --csv --log-file gpurun_out/counters32_$TAG.csv python bench.py --steps 1 --warmup 1 --only-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-c32 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:flux_kernel -s 3 -c 6 -o gpurun_out/prof_full_$TAG python bench.py --n 128 --steps 1 --warmup 1 --no-fp32 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu-full rc=$?
