@@ -823,7 +823,10 @@ int or_run(const or_gas* g, const or_grid* gr, double* q, int nsteps, double dt_
  *   zeta  = 1/(rho0 Omega) sum 1/2 rho |omega|^2 dV, omega = curl U    (O-24)
  *   eps_s = mu/(rho0 Omega) sum omega.omega dV                         (first term)
  *   eps_d = 4/3 mu/(rho0 Omega) sum (div U)^2 dV                       (second term)
- * plus the conservation monitors sum rho dV, sum rho U dV (3), sum rho E dV and Omega.
+ * plus the conservation monitors sum rho dV, sum rho U dV (3), sum rho E dV and Omega, and
+ *   Pi    = 1/(rho0 Omega) sum p div U dV                               (pressure-dilatation)
+ * which closes the kinetic-energy budget of compressible decaying turbulence,
+ * dE_k/dt = Pi - eps_s - eps_d (constant mu; the paper's eps_com = eps_s + eps_d).
  * Velocity derivatives at a cell centre (O-25): the fourth-order central difference in the cell
  * index of the cell-average velocities, times the metric J = d(index)/dx at the cell centre:
  *   du/dx_d (j) = J(j + 1/2) [8 (u_{j+1} - u_{j-1}) - (u_{j+2} - u_{j-2})] / 12.
@@ -868,6 +871,8 @@ void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double
         for (int c = 0; c < 3; ++c) acc[OR_DIAG_MOM_X + c] += qg[gidx(gr, 1 + c, i, j, k)] * vol;
         acc[OR_DIAG_ENERGY] += qg[gidx(gr, 4, i, j, k)] * vol;
         acc[OR_DIAG_VOLUME] += vol;
+        double p = (g->gamma - 1.0) * (qg[gidx(gr, 4, i, j, k)] - 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
+        acc[OR_DIAG_PDIL] += p * dv * vol;
       }
   double omega = acc[OR_DIAG_VOLUME];
   for (int v = 0; v < OR_NDIAG; ++v) out[v] = acc[v];
@@ -875,6 +880,7 @@ void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double
   out[OR_DIAG_ENSTROPHY] = acc[OR_DIAG_ENSTROPHY] / (rho0 * omega);
   out[OR_DIAG_EPS_S] = g->mu_ref * acc[OR_DIAG_EPS_S] / (rho0 * omega);
   out[OR_DIAG_EPS_D] = 4.0 / 3.0 * g->mu_ref * acc[OR_DIAG_EPS_D] / (rho0 * omega);
+  out[OR_DIAG_PDIL] = acc[OR_DIAG_PDIL] / (rho0 * omega);
 }
 
 /* ------------------------------------------------------------------------------------------

@@ -164,10 +164,11 @@ void or_plane_stats(const or_gas* g, const or_grid* gr, const double* q, double*
  * derivatives by O-25 (fourth-order central in the cell index times J at the cell centre).
  * Pins (test_oracle_diagnostics.py): TGV closed forms E_k = 1/8, zeta = 3/8 kappa(h)^2 with
  * kappa(h) = (8 sin h - sin 2h)/(6h) the exact symbol of the difference, div U = 0; a potential
- * flow (omega = 0, eps_d closed form); a linear shear on a tanh-stretched axis (metric); Omega. */
-#define OR_NDIAG 10
+ * flow (omega = 0, eps_d closed form); a linear shear on a tanh-stretched axis (metric); Omega;
+ * the pressure-dilatation of a potential flow with a harmonic pressure (closed form). */
+#define OR_NDIAG 11
 enum { OR_DIAG_EK = 0, OR_DIAG_ENSTROPHY, OR_DIAG_EPS_S, OR_DIAG_EPS_D, OR_DIAG_MASS, OR_DIAG_MOM_X,
-       OR_DIAG_MOM_Y, OR_DIAG_MOM_Z, OR_DIAG_ENERGY, OR_DIAG_VOLUME };
+       OR_DIAG_MOM_Y, OR_DIAG_MOM_Z, OR_DIAG_ENERGY, OR_DIAG_VOLUME, OR_DIAG_PDIL };
 void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double rho0, double out[OR_NDIAG]);
 
 int or_num_threads(void);

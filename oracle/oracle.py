@@ -260,7 +260,8 @@ def run(gas: Gas, q: np.ndarray, dx, nsteps: int, dt_fixed: float = 0.0, cfl: fl
     return q, hist[:nsteps]
 
 
-DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
+DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume",
+              "p_dil")
 
 
 def diagnostics(gas: Gas, q: np.ndarray | None = None, dx=None, rho0: float = 1.0, qg: np.ndarray | None = None,

@@ -16,7 +16,7 @@ import pytest
 from oracle import oracle as O
 from paper_2207_01173_b200 import inputs
 
-E, Z, ES, ED, MASS, MX, MY, MZ, EN, VOL = range(10)
+E, Z, ES, ED, MASS, MX, MY, MZ, EN, VOL, PDIL = range(11)
 
 
 def kappa(h):
@@ -74,6 +74,24 @@ def test_potential_flow():
     d = O.diagnostics(O.make_gas(mu=0.3), q, (h, h, h))
     assert d[ES] == 0.0 and d[Z] == 0.0
     assert d[ED] == pytest.approx(4 / 3 * 0.3 * kappa(h) ** 2 / 2, rel=1e-13)
+    assert abs(d[PDIL]) < 1e-14  # uniform p: mean of div U = kappa mean(cos x) = 0
+
+
+@pytest.mark.parametrize("n", [8, 10, 13])
+def test_pressure_dilatation_closed_form(n):
+    """U = sin x, p = 1 + 0.5 cos x, rho = 1.3: the discrete div U is kappa(h) cos x exactly, so
+    sum p div U dV / Omega = kappa (mean cos x + 0.5 mean cos^2 x) = kappa/4 (discrete orthogonality,
+    n >= 3), and Pi = kappa/(4 rho0).  A dropped (gamma - 1), a kinetic-energy slip in p or a wrong
+    sign all fail."""
+    h = 2 * math.pi / n
+    x = inputs.cell_centres(n, -math.pi, math.pi)
+    U = np.broadcast_to(np.sin(x), (n, n, n))
+    p = np.broadcast_to(1.0 + 0.5 * np.cos(x), (n, n, n))
+    q = inputs.prim_to_cons(np.full((n, n, n), 1.3), U, 0 * U, 0 * U, p)
+    d = O.diagnostics(O.make_gas(mu=0.0), q, (h, h, h), rho0=1.3)
+    assert d[PDIL] == pytest.approx(kappa(h) / 4 / 1.3, rel=1e-12)
+    d2 = O.diagnostics(O.make_gas(mu=0.0), q, (h, h, h), rho0=1.0)
+    assert d2[PDIL] == pytest.approx(kappa(h) / 4, rel=1e-12)
 
 
 def test_linear_shear_on_tanh_axis():
