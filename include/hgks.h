@@ -144,16 +144,18 @@ const char* hgks_last_error(const hgks_ctx* c);
  *   out[HGKS_DIAG_EPS_D]     4/3 mu/(rho0 Omega) sum (div U)^2 dV      (eps_com, second term)
  *   out[HGKS_DIAG_MASS..ENERGY]  sum rho dV, sum rho U dV (x, y, z), sum rho E dV
  *   out[HGKS_DIAG_VOLUME]    Omega = sum dV
+ *   out[HGKS_DIAG_PDIL]      Pi = 1/(rho0 Omega) sum p div U dV  (pressure-dilatation; with the two
+ *                            eps_com terms it closes dE_k/dt = Pi - eps_s - eps_d)
  * mu = params.mu_ref.  Velocity derivatives: fourth-order central difference in the cell index
  * times d(index)/dx at the cell centre, ghosts as the step fills them (periodic, wall mirror,
  * halo).  Computed in fp64 for either precision by a fixed-order (deterministic) two-pass
  * reduction, then an NCCL sum over ranks.  rho0 > 0.  Synchronises the stream.
  * Errors: HGKS_EINVAL (NULL, no state, rho0 <= 0), HGKS_ECUDA, HGKS_ENCCL. */
-#define HGKS_DIAG_COUNT 10
+#define HGKS_DIAG_COUNT 11
 typedef enum {
   HGKS_DIAG_EK = 0, HGKS_DIAG_ENSTROPHY = 1, HGKS_DIAG_EPS_S = 2, HGKS_DIAG_EPS_D = 3,
   HGKS_DIAG_MASS = 4, HGKS_DIAG_MOM_X = 5, HGKS_DIAG_MOM_Y = 6, HGKS_DIAG_MOM_Z = 7,
-  HGKS_DIAG_ENERGY = 8, HGKS_DIAG_VOLUME = 9
+  HGKS_DIAG_ENERGY = 8, HGKS_DIAG_VOLUME = 9, HGKS_DIAG_PDIL = 10
 } hgks_diag;
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]);
 

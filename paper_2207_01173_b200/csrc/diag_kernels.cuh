@@ -1,7 +1,8 @@
 // diag_kernels.cuh — on-device volume diagnostics (O-24, O-25).
 //
-//   diag_kernel<T>      per-cell terms of E_k, enstrophy, |omega|^2, (div U)^2 and the conservation
-//                       monitors, summed per block in a fixed order (fp64 for either precision)
+//   diag_kernel<T>      per-cell terms of E_k, enstrophy, |omega|^2, (div U)^2, p div U and the
+//                       conservation monitors, summed per block in a fixed order (fp64 for either
+//                       precision)
 //   diag_final_kernel   one block: fixed-order sum of the block partials -> NDIAG doubles
 //
 // Deterministic: a fixed grid (DIAG_BLOCKS x DIAG_TPB), a fixed grid-stride cell order per thread
@@ -11,7 +12,7 @@
 
 namespace hgks {
 
-constexpr int NDIAG = 10;  // HGKS_DIAG_COUNT
+constexpr int NDIAG = 11;  // HGKS_DIAG_COUNT
 constexpr int DIAG_BLOCKS = 148 * 4;
 
 template <typename T>
@@ -20,7 +21,7 @@ __device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q, Geo<T> g, DiagGeo dg,
+__global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q, Geo<T> g, DiagGeo dg, double gamma,
                                                         double* __restrict__ partial) {
   __shared__ double sh[NDIAG * DIAG_TPB];
   double acc[NDIAG];
@@ -63,8 +64,11 @@ __global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q,
     acc[5] += m[0] * vol;
     acc[6] += m[1] * vol;
     acc[7] += m[2] * vol;
-    acc[8] += (double)q[qidx(g, 4, i, j, k)] * vol;
+    const double rhoE = (double)q[qidx(g, 4, i, j, k)];
+    acc[8] += rhoE * vol;
     acc[9] += vol;
+    const double p = (gamma - 1.0) * (rhoE - 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
+    acc[10] += p * dv * vol;  // pressure-dilatation
   }
   block_sum_fixed(acc, sh);
   if (threadIdx.x == 0) {

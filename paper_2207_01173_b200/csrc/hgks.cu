@@ -529,7 +529,7 @@ static int diagnostics_t(hgks_ctx* c) {
   if ((rc = fill_ghosts<T>(c, Q, true))) return rc;
   const DiagGeo dg = diag_geo(c);
   double* out = c->diag_dev + DIAG_BLOCKS * NDIAG;
-  diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->diag_dev);
+  diag_kernel<T><<<DIAG_BLOCKS, DIAG_TPB, 0, c->s>>>(Q, g, dg, c->p.gamma, c->diag_dev);
   diag_final_kernel<NDIAG><<<1, DIAG_TPB, 0, c->s>>>(c->diag_dev, DIAG_BLOCKS, out);
   c->total_launches += 2;
   CUDA_TRY(c, cudaGetLastError());
@@ -906,10 +906,18 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   h->bad_cell = ~0ull;
   CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
   const int cur0 = c->cur;
-  int rc = c->fp32 ? run_steps<float>(c, nsteps) : run_steps<double>(c, nsteps);
-  if (rc) return rc;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  // With a t_end the run may halt early (every later kernel then returns at once): enqueue in
+  // chunks and read the halt word between them, so a generous nsteps costs no idle launches.
+  // Without t_end everything is enqueued at once (a halt then only follows an invalid state).
+  const int chunk = t_end > 0.0 ? 16 : (nsteps > 0 ? nsteps : 1);
+  for (int done = 0; done < nsteps || done == 0; done += chunk) {
+    const int n = std::min(chunk, nsteps - done);
+    int rc = c->fp32 ? run_steps<float>(c, n) : run_steps<double>(c, n);
+    if (rc) return rc;
+    CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(c, cudaStreamSynchronize(c->s));
+    if (h->halt || n <= 0) break;
+  }
   c->cur = cur0 ^ (int)(h->steps_done & 1);  // buffer holding the last committed state
   *t_inout = h->t;
   if (dt_last) *dt_last = h->dt_last;
@@ -945,6 +953,7 @@ int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
   out[HGKS_DIAG_ENSTROPHY] = a[HGKS_DIAG_ENSTROPHY] / (rho0 * vol);
   out[HGKS_DIAG_EPS_S] = mu * a[HGKS_DIAG_EPS_S] / (rho0 * vol);
   out[HGKS_DIAG_EPS_D] = 4.0 / 3.0 * mu * a[HGKS_DIAG_EPS_D] / (rho0 * vol);
+  out[HGKS_DIAG_PDIL] = a[HGKS_DIAG_PDIL] / (rho0 * vol);
   return HGKS_OK;
 }
 

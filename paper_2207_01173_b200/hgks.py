@@ -31,7 +31,8 @@ EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
             "hgks_diagnostics", "hgks_plane_stats", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
 STAT_NAMES = ("rho", "U", "V", "W", "UU", "VV", "WW", "UV", "rhoU", "rhoV", "rhoUV", "c", "M", "MM", "T", "p")
-DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume")
+DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume",
+              "p_dil")
 
 
 class HgksError(RuntimeError):

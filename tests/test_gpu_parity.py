@@ -259,6 +259,47 @@ def test_t_end_clamp():
         assert s.t == pytest.approx(0.05, rel=1e-14)
 
 
+def test_t_end_many_steps_chunked():
+    """hgks_step with a t_end enqueues in chunks and stops at the halt: a huge nsteps costs nothing,
+    and splitting the call anywhere gives the same bits (same dt sequence, same commits)."""
+    import time
+    q, dx = inputs.tgv(16)
+    with _tgv_solver(16, cfl=0.4) as a, _tgv_solver(16, cfl=0.4) as b:
+        a.set_state(q)
+        b.set_state(q)
+        t0 = time.perf_counter()
+        a.step(1_000_000, t_end=0.5)  # ~35 steps, several chunks
+        assert time.perf_counter() - t0 < 20.0
+        b.step(5, t_end=0.5)
+        b.step(17, t_end=0.5)
+        b.step(1_000_000, t_end=0.5)
+        assert a.t == pytest.approx(0.5, rel=1e-14) and b.t == a.t
+        assert np.array_equal(a.get_state(), b.get_state())
+
+
+def test_full_size_tgv512_sampled_parity():
+    """BASELINE config 5 size on one GPU (5.4 GB per state): one CFL step at 512^3 fp64, sampled
+    cells against the oracle; dt against Table 3's 512^3 value (4.462e-4)."""
+    n = 512
+    q, dx = inputs.tgv(n)
+    with _tgv_solver(n, cfl=0.4) as s:
+        s.set_state(q)
+        dt = s.step(1)
+        q1 = s.get_state()
+    gas = O.make_gas(mu=TGV["mu"])
+    dt_o = O.cfl_dt(gas, q, dx, 0.4)
+    assert dt == pytest.approx(dt_o, rel=1e-13)
+    assert dt_o == pytest.approx(4.462e-4, rel=1e-3)
+    rng = np.random.default_rng(512)
+    cells = [(0, 0, 0), (n - 1, n - 1, n - 1), (n // 2, n - 1, 1)]
+    cells += [tuple(int(x) for x in rng.integers(0, n, 3)) for _ in range(9)]
+    den = np.array([np.abs(q1[0]).max(), *[np.sqrt((q1[1:4] ** 2).sum(0)).max()] * 3, np.abs(q1[4]).max()])
+    for c in cells:
+        ref = _oracle_one_step_at(q, dx, dt_o, gas, c)
+        got = q1[:, c[2], c[1], c[0]]
+        assert (np.abs(got - ref) / den).max() <= 1e-11, (c, got, ref)
+
+
 def _oracle_one_step_at(qfull, dx, dt, gas, cell):
     """Exact oracle value of one full S2O4 step at one cell of a periodic field, from the
     13^3 neighbourhood it depends on (stage-1 operator on 7^3, stage-2 operator at the cell)."""
