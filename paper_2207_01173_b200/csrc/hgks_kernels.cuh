@@ -348,8 +348,14 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
 #ifdef HGKS_PHASE_TIMING
     long long tp0 = clock64();
 #endif
+#ifndef HGKS_DEBUG_SKIP_AB
+#define HGKS_DEBUG_SKIP_AB 0  // timing experiment only: phases A/B run for the first face alone
+#endif
+    const bool do_ab = !HGKS_DEBUG_SKIP_AB || it == 0;
+    if (do_ab) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();  // sA(fn) landed; every thread is done with sB of the previous face
+    }
 #ifdef HGKS_PHASE_TIMING
     long long tp1 = clock64();
 #endif
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
   // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
   // One item = (a, c, l2) computes both Gauss abscissae m = 0, 1 from the same 30 loads: point
   // m = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
-  for (int w = threadIdx.x; w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
+  for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
     const int c = (w / TT1) % 5;
     const int l2 = w / (TT1 * 5);
@@ -389,8 +395,10 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, HGKS_FLUX_MINB)
       dst[k * SB_K + TT1] = o1[k];
     }
   }
+  if (do_ab) {
   __syncthreads();  // sB complete; sA free for the next face
-  if (it + 1 < nfn) issue_A(fn + 1);
+  if (it + 1 < nfn && !HGKS_DEBUG_SKIP_AB) issue_A(fn + 1);
+  }
 #ifdef HGKS_PHASE_TIMING
   long long tp2 = clock64();
 #endif
