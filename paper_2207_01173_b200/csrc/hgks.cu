@@ -436,39 +436,60 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     attr_done[pi][STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  // Two streams: the reconstruction sweep of direction d+1 (memory-bound) runs on s2 while the
-  // flux sweep of direction d (FP64-bound) runs on s.  FF[d % 2] is written by recon d and read
-  // by flux d; recon d+2 waits for flux d before reusing the buffer.
-  // stage input: x/y ghosts written (ev_xy, recorded by fill_ghosts on c->s); z ghosts land on
-  // c->sc (ev_halo).  The x sweep's face lines of the interior z planes need no z ghost, so they
-  // run while the halo is in flight; its ghost-plane lines (z = -2, -1, nz, nz+1) and every
+  // Two streams: the reconstruction sweep of the next direction (memory-bound) runs on s2 while the
+  // flux sweep of the current one (FP64-bound) runs on s.  Face-field buffer FF[pos & 1] by position
+  // in the sweep order; recon(pos 2) waits for flux(pos 0) before reusing its buffer.  recon(pos 1)
+  // becomes ready together with flux(pos 0) and floods the SMs first, delaying that flux kernel by
+  // about its own duration; recon(pos 2) starts behind flux(pos 1) and costs it little (measured:
+  // the delay follows the position, not the direction -- y, x, z moved it from the x to the y flux).
+  // Stage input: x/y ghosts written (ev_xy, recorded by fill_ghosts on c->s); z ghosts land on
+  // c->sc (ev_halo).  The first sweep's face lines of the interior z planes need no z ghost, so
+  // they run while the halo is in flight; its ghost-plane lines (z = -2, -1, nz, nz+1) and every
   // later sweep wait for ev_halo.
+#ifndef HGKS_SWEEP_ORDER
+#define HGKS_SWEEP_ORDER 0  // 0: x, y, z ; 1: y, x, z
+#endif
+  const int order[3] = {HGKS_SWEEP_ORDER ? 1 : 0, HGKS_SWEEP_ORDER ? 0 : 1, 2};
+  int pos_of[3];
+  for (int k = 0; k < 3; ++k) pos_of[order[k]] = k;
   CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_xy, 0));
   const int n3[3] = {nx, ny, nz};
-  // lines of the x sweep: (t1 = y, t2 = z), t1 fastest; interior z planes = one contiguous range
-  const long long w0 = ff_pitch(ny, (int)sizeof(T)), nl0 = w0 * (nz + 4);
+  auto ffbuf = [&](int d) { return (T*)c->FF[pos_of[d] & 1]; };
   auto recon_launch = [&](int d, long long lbeg, long long lcnt, long long gap_at, long long gap) {
-    T* ff = (T*)c->FF[d & 1];
-    const int blocks = (int)((5 * lcnt + 127) / 128);
+    T* ff = ffbuf(d);
     const LineRange lr{lbeg, lcnt, gap_at, gap};
-    if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
-    if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    if (d == 1) {  // y sweep: z-fastest face-field lines, lr ranges over z
+      dim3 grid((unsigned)((lcnt + RZ_Z - 1) / RZ_Z), (nx + 4 + RZ_X - 1) / RZ_X, 5);
+      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    } else {
+      const int blocks = (int)((5 * lcnt + 127) / 128);
+      if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+      if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+    }
     c->total_launches += 1;
   };
   auto recon = [&](int d) -> int {
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
     const long long nl = (long long)ff_pitch(n1, (int)sizeof(T)) * (n2 + 4);
     prof_begin(c, HGKS_K_RECON, c->s2);
-    if (d == 0) {
-      recon_launch(0, 2 * w0, (long long)nz * w0, nl0, 0);                 // interior z planes
+    if (pos_of[d] == 0) {  // first sweep: interior z lines, then (after the halo) the ghost-plane ones
+      if (d == 1) {
+        recon_launch(1, 0, nz, nz, 0);
+      } else {  // x sweep lines (t1 = y, t2 = z): interior z planes are one contiguous range
+        const long long w0 = ff_pitch(ny, (int)sizeof(T));
+        recon_launch(0, 2 * w0, (long long)nz * w0, nl, 0);
+      }
       prof_end(c, HGKS_K_RECON, c->s2);
       CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_halo, 0));
       prof_begin(c, HGKS_K_RECON, c->s2);
-      recon_launch(0, 0, 4 * w0, 2 * w0, (long long)nz * w0);              // the 4 ghost planes
-    } else if (d == 1) {  // y sweep: z-fastest face-field lines
-      dim3 grid((nz + 4 + RZ_Z - 1) / RZ_Z, (nx + 4 + RZ_X - 1) / RZ_X, 5);
-      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, (T*)c->FF[1], g, c->ctl);
-      c->total_launches += 1;
+      if (d == 1) {
+        recon_launch(1, -2, 4, 2, nz);
+      } else {
+        const long long w0 = ff_pitch(ny, (int)sizeof(T));
+        recon_launch(0, 0, 4 * w0, 2 * w0, (long long)nz * w0);
+      }
+    } else if (d == 1) {
+      recon_launch(1, -2, nz + 4, nz + 4, 0);
     } else {
       recon_launch(d, 0, nl, nl, 0);
     }
@@ -477,7 +498,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     return HGKS_OK;
   };
   auto flux = [&](int d) -> int {
-    T* ff = (T*)c->FF[d & 1];
+    T* ff = ffbuf(d);
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
     // faces per block along the normal: HGKS_FLUX_TPB (measured best at 256^3: 16 > 8 > 4 > 2), halved
     // while the grid would have fewer than 8 blocks per SM
@@ -500,9 +521,9 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   };
   // enqueue order matters: an event must be recorded before a wait on it is enqueued
   int rc;
-  if ((rc = recon(0)) || (rc = recon(1)) || (rc = flux(0))) return rc;
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_flux[0], 0));  // FF[0] free again
-  if ((rc = recon(2)) || (rc = flux(1)) || (rc = flux(2))) return rc;
+  if ((rc = recon(order[0])) || (rc = recon(order[1])) || (rc = flux(order[0]))) return rc;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_flux[order[0]], 0));  // its face-field buffer is free again
+  if ((rc = recon(order[2])) || (rc = flux(order[1])) || (rc = flux(order[2]))) return rc;
   c->total_launches += 3;
   CUDA_TRY(c, cudaGetLastError());
   return HGKS_OK;

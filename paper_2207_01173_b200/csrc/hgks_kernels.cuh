@@ -222,15 +222,19 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
 // Measured against a shared-memory transpose (32 x by 8/16/24 z per block): the transpose blocks
 // hold shared memory and barriers, and slow the concurrent x-sweep flux kernel more than they gain.
 constexpr int RZ_Z = 32, RZ_X = 4;
+// Lines (z, x) with z from the range zr (lbeg + j, j in [0, lcnt), skipping gap after gap_at: the
+// interior z lines run while the z halo is in flight, the 4 ghost-plane z lines after it).
 template <typename T>
 __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
-                                                                const Ctl* __restrict__ ctl) {
+                                                                const Ctl* __restrict__ ctl, LineRange zr) {
   if (ctl->halt) return;
   const FFLayout<T, 1> L = ff_layout<T, 1>(g);
   const int tz = threadIdx.x % RZ_Z, tx = threadIdx.x / RZ_Z;
   const int c = blockIdx.z;
-  const int z = blockIdx.x * RZ_Z + tz - 2, x = blockIdx.y * RZ_X + tx - 2;
-  if (z >= g.n[2] + 2 || x >= g.n[0] + 2) return;
+  const long long jz = (long long)blockIdx.x * RZ_Z + tz;
+  const int x = blockIdx.y * RZ_X + tx - 2;
+  if (jz >= zr.lcnt || x >= g.n[0] + 2) return;
+  const int z = (int)(zr.lbeg + jz + (jz >= zr.gap_at ? zr.gap : 0));
   const int gv = (c == 0) ? 0 : (c == 4 ? 4 : (c == 1 ? 2 : (c == 2 ? 3 : 1)));  // (V, W, U) frame (O-23)
   const long long sN = g.px;
   const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + (long long)z * g.plane + x;
