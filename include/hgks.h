@@ -128,7 +128,9 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
 /* Copy out this rank's slab in the set_state layout (fp64; host or device pointer). Synchronises. */
 int hgks_get_state(hgks_ctx* c, double* q, int on_device);
 
-/* Release everything owned by c.  NULL-safe. */
+/* Release everything owned by c.  NULL-safe.  Collective like every call: a loopback-group rank
+ * waits (host barrier) until every rank of the group has entered hgks_destroy, so no rank frees
+ * buffers or events a peer is still using. */
 int hgks_destroy(hgks_ctx* c);
 
 /* Last error message of c (or of the calling thread when c == NULL); never NULL. */

@@ -397,14 +397,13 @@ static void lb_leave(hgks_ctx* c) {
 template <typename T>
 static int fill_ghosts(hgks_ctx* c, T* q, bool wait_halo) {
   Geo<T> g = make_geo<T>(c);
-  long long total = (long long)g.n[2] * g.plane;
   prof_begin(c, HGKS_K_GHOST);
   if (g.wall[0] || g.wall[1]) {
     ghost_wall_kernel<T><<<blocks_for((long long)g.n[2] * 6 * std::max(g.n[0], g.n[1]), 256), 256, 0, c->s>>>(
         q, g, c->p.gamma, c->ctl);
     c->total_launches += 1;
   }
-  ghost_xy_kernel<T><<<blocks_for(total, 256), 256, 0, c->s>>>(q, g, c->ctl);
+  ghost_xy_kernel<T><<<blocks_for((long long)g.n[2] * 5 * (6LL * g.px + 6LL * g.n[1]), 256), 256, 0, c->s>>>(q, g, c->ctl);
   prof_end(c, HGKS_K_GHOST);
   c->total_launches += 1;
   CUDA_TRY(c, cudaGetLastError());
@@ -1023,6 +1022,10 @@ int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* 
 int hgks_destroy(hgks_ctx* c) {
   if (!c) return HGKS_OK;
   cudaSetDevice(c->dev);
+  // loopback group: destroy is collective -- a rank returning from its last collective may still
+  // be followed by peers that read its context (event handles) on the host, so nobody frees
+  // anything until every rank has entered destroy (a timeout only delays the teardown)
+  if (c->grp) c->grp->barrier();
   if (c->s) cudaStreamSynchronize(c->s);
   if (c->sc) cudaStreamSynchronize(c->sc);
   if (c->comm) ncclCommDestroy(c->comm);

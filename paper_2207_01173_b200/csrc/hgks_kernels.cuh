@@ -575,19 +575,30 @@ __global__ void ghost_wall_kernel(T* __restrict__ q, Geo<T> g, double gamma, con
 template <typename T>
 __global__ void ghost_xy_kernel(T* __restrict__ q, Geo<T> g, const Ctl* __restrict__ ctl) {
   if (ctl->halt) return;
-  const long long total = (long long)g.n[2] * 5 * (g.py) * (g.px);
+  // only the ghost cells of each (plane, variable): the 3-deep bands j < 0, j >= ny over the full
+  // extended x range (6 px cells), then the x bands i < 0, i >= nx of the interior rows (6 ny)
   const int nx = g.n[0], ny = g.n[1];
+  const long long per = 6LL * g.px + 6LL * ny;
+  const long long total = (long long)g.n[2] * 5 * per;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int ii = (int)(e % g.px);
-    long long r = e / g.px;
-    const int jj = (int)(r % g.py);
-    r /= g.py;
-    const int v = (int)(r % 5);
-    const int k = (int)(r / 5);
-    const int i = ii - 3, j = jj - 3;
+    const long long r = e % per;
+    const long long kv = e / per;
+    const int v = (int)(kv % 5);
+    const int k = (int)(kv / 5);
+    int i, j;
+    if (r < 6LL * g.px) {
+      const int jj = (int)(r / g.px);
+      j = jj < 3 ? jj - 3 : ny + jj - 3;
+      i = (int)(r % g.px) - 3;
+    } else {
+      const int rr = (int)(r - 6LL * g.px);
+      const int ii = rr % 6;
+      j = rr / 6;
+      i = ii < 3 ? ii - 3 : nx + ii - 3;
+    }
     // source: wrap the periodic in-plane axes only (wall ghosts come from ghost_wall_kernel)
     const int si = g.wall[0] ? i : (i + nx) % nx, sj = g.wall[1] ? j : (j + ny) % ny;  // n >= 5 > 3
-    if (si == i && sj == j) continue;  // interior cell, or a pure wall ghost
+    if (si == i && sj == j) continue;  // a pure wall ghost
     q[qidx(g, v, i, j, k)] = q[qidx(g, v, si, sj, k)];
   }
 }
