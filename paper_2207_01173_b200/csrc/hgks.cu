@@ -85,6 +85,7 @@ struct hgks_ctx {
   // loopback group (params.group_key): ordering events of the halo copies and the reductions
   cudaEvent_t lb_post = nullptr, lb_done = nullptr, lb_rpost = nullptr, lb_rdone = nullptr;
   LoopGroup* grp = nullptr;
+  bool flux_attr_set[2] = {false, false};  // max dynamic shared memory set for the stage-1/2 flux kernels
   void* red_tmp = nullptr;            // loopback reduction result before the in-place write-back
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   Ctl* ctl = nullptr;
@@ -422,9 +423,8 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   Geo<T> g = make_geo<T>(c);
   GasK<T> gas = make_gas<T>(c->p);
   const size_t smem = flux_smem_bytes<T>();
-  static bool attr_done[2][2] = {{false, false}, {false, false}};
-  const int pi = sizeof(T) == 8 ? 0 : 1;
-  if (!attr_done[pi][STAGE - 1]) {
+  // function attributes belong to the device: kept per context (one device each), not process-wide
+  if (!c->flux_attr_set[STAGE - 1]) {
     const int sm = (int)smem;
     CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -432,7 +432,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    attr_done[pi][STAGE - 1] = true;
+    c->flux_attr_set[STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   // Two streams: the reconstruction sweep of the next direction (memory-bound) runs on s2 while the
