@@ -564,7 +564,8 @@ static int run_steps(hgks_ctx* c, int nsteps) {
   Geo<T> g = make_geo<T>(c);
   const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   const int tpb = 256;
-  const int ublocks = (int)((ncell + tpb - 1) / tpb);
+  const dim3 ugrid((g.n[0] + UPD_X - 1) / UPD_X, (g.n[1] + UPD_Y - 1) / UPD_Y, g.n[2]);
+  const int ublocks = (int)(ugrid.x * ugrid.y * ugrid.z);
   const DiagGeo dg = diag_geo(c);
   const bool bulk = c->p.force_mode == HGKS_FORCE_BULK;
   int rc;
@@ -580,14 +581,14 @@ static int run_steps(hgks_ctx* c, int nsteps) {
     if ((rc = fill_ghosts<T>(c, Qn, false))) return rc;
     if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
-    update_kernel<T, 1><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
+    update_kernel<T, 1><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
                                                    c->ctl, c->bulk_dev);
     prof_end(c, HGKS_K_UPDATE);
     // stage 2 at Q* (same dt and windows, O-11)
     if ((rc = fill_ghosts<T>(c, Qs, false))) return rc;
     if ((rc = flux_sweeps<T, 2>(c, Qs))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
-    update_kernel<T, 2><<<ublocks, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
+    update_kernel<T, 2><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
                                                    c->ctl, c->bulk_dev);
     prof_end(c, HGKS_K_UPDATE);
     c->total_launches += 2;
@@ -769,7 +770,7 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     free(hd);
     ok = ok && cudaMalloc(&c->diag_dev, (DIAG_BLOCKS + 1) * NDIAG * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->diag_host, NDIAG * sizeof(double)) == cudaSuccess;
-    const size_t ublocks = ((size_t)nloc[0] * nloc[1] * nloc[2] + DIAG_TPB - 1) / DIAG_TPB;
+    const size_t ublocks = (size_t)((nloc[0] + UPD_X - 1) / UPD_X) * ((nloc[1] + UPD_Y - 1) / UPD_Y) * nloc[2];
     ok = ok && cudaMalloc(&c->bulk_dev, 2 * ublocks * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->stats_dev, (size_t)nloc[1] * NSTAT * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->metric, tot * c->esz) == cudaSuccess;

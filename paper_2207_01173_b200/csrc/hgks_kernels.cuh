@@ -635,21 +635,21 @@ __device__ __forceinline__ void block_max_commit(double s, unsigned long long* d
 // Lt = L + dt/2 dL of Q^n, recovered from the two stage-1 outputs: with a = Q* - Q^n and
 // b = R - Q^n (a = dt L/2 + dt^2 dL/8, b = dt L + dt^2 dL/6), Lt = (8a - 3b)/dt.  Mode 2 also
 // sums (rho dV, rho U dV) of Q^{n+1} per block (fixed order) into bulk[2 * blockIdx.x + {0, 1}].
+constexpr int UPD_X = 64, UPD_Y = DIAG_TPB / UPD_X;  // update_kernel block shape (DIAG_TPB threads)
 template <typename T, int STAGE>
 __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
                               Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk) {
   if (ctl->halt) return;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  const long long ncell = (long long)nx * ny * nz;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // block = UPD_X x UPD_Y cells of one z plane (grid: x tiles, y tiles, z): no index divisions
+  const int i = blockIdx.x * UPD_X + (threadIdx.x % UPD_X);
+  const int j = blockIdx.y * UPD_Y + (threadIdx.x / UPD_X);
+  const int k = blockIdx.z;
   const double dt = ctl->dt;
   const int fmode = ctl->force_mode;
   double smax = 0.0, bsum[2] = {0.0, 0.0};
-  if (e < ncell) {
-    const int i = (int)(e % nx);
-    const int j = (int)((e / nx) % ny);
-    const int k = (int)(e / ((long long)nx * ny));
+  if (i < nx && j < ny) {
     const long long nfx = (long long)(nx + 1) * ny * nz, nfy = (long long)nx * (ny + 1) * nz, nfz = (long long)nx * ny * (nz + 1);
     const long long ix = ((long long)k * ny + j) * (nx + 1) + i;
     const long long iy = ((long long)k * (ny + 1) + j) * nx + i;
@@ -723,8 +723,9 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
       __shared__ double sh[2 * DIAG_TPB];
       block_sum_fixed(bsum, sh);
       if (threadIdx.x == 0) {
-        bulk[2 * blockIdx.x] = bsum[0];
-        bulk[2 * blockIdx.x + 1] = bsum[1];
+        const long long bid = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        bulk[2 * bid] = bsum[0];
+        bulk[2 * bid + 1] = bsum[1];
       }
     }
   }
