@@ -290,8 +290,11 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, sizeof(T) == 4 ? HGKS_FLUX_MINB
   const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2;
   // fpb consecutive normal faces per block: the face fields of face fn+1 are copied
   // (cp.async) into sA while face fn is in phase C, so only the first copy's latency is exposed
-  const int fn0 = blockIdx.z * fpb;
-  const int nfn = min(fpb, g.n[DIR] + 1 - fn0);
+  // gridDim.z blocks share the n+1 normal faces as evenly as possible (fpb or fpb - 1 each)
+  const int nf_all = g.n[DIR] + 1;
+  const int fn0 = (int)(((long long)blockIdx.z * nf_all) / gridDim.z);
+  const int nfn = (int)(((long long)(blockIdx.z + 1) * nf_all) / gridDim.z) - fn0;
+  (void)fpb;
   auto issue_A = [&](int fn) {
     const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
     const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
