@@ -499,11 +499,22 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   auto flux = [&](int d) -> int {
     T* ff = ffbuf(d);
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    // faces per block along the normal: HGKS_FLUX_TPB (measured best at 256^3: 16 > 8 > 4 > 2), halved
-    // while the grid would have fewer than 8 blocks per SM
+    // faces per block along the normal: at most HGKS_FLUX_TPB (measured at 256^3: 16 > 8 > 4 > 2 by
+    // 0.4 % / 1 % / 2 %), chosen to balance that against the last partial wave of blocks (thin
+    // slabs: 256 x 256 x 32 gives 7.35 waves at 16 faces per block, 14.7 at 8)
     const long long tiles = (long long)((n1 + TT1 - 1) / TT1) * ((n2 + TT2 - 1) / TT2);
+    const double slots = 148.0 * (sizeof(T) == 4 ? HGKS_FLUX_MINB32 : HGKS_FLUX_MINB);
     int fpb = HGKS_FLUX_TPB;
-    while (fpb > 2 && tiles * ((n3[d] + 1 + fpb - 1) / fpb) < 148LL * 8) fpb /= 2;
+    double best = -1.0;
+    for (int f = HGKS_FLUX_TPB; f >= 2; f /= 2) {
+      const double waves = (double)(tiles * ((n3[d] + 1 + f - 1) / f)) / slots;
+      const double face_eff = f >= 16 ? 1.0 : (f >= 8 ? 0.996 : (f >= 4 ? 0.99 : 0.98));
+      const double eff = face_eff * waves / std::ceil(waves);
+      if (eff > best + 1e-9) {
+        best = eff;
+        fpb = f;
+      }
+    }
     dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, (n3[d] + 1 + fpb - 1) / fpb);
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
