@@ -454,16 +454,29 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_xy, 0));
   const int n3[3] = {nx, ny, nz};
   auto ffbuf = [&](int d) { return (T*)c->FF[pos_of[d] & 1]; };
+  // Each reconstruction thread marches along the normal; on thin slabs (few lines) the march is
+  // split into segments (>= 16 faces each) so a launch still has ~HGKS_RECON_THREADS threads.
+#ifndef HGKS_RECON_THREADS
+#define HGKS_RECON_THREADS 1500000  // measured: 1 (no split) < 6e5 < 1.5e6 ~ 3e6 ~ 8e6
+#endif
+  auto segments = [&](int d, long long nthreads) {
+    const int nf = n3[d] + 1;
+    const long long want = (HGKS_RECON_THREADS + nthreads - 1) / nthreads;
+    return (int)std::max<long long>(1, std::min<long long>(want, nf / 16));
+  };
   auto recon_launch = [&](int d, long long lbeg, long long lcnt, long long gap_at, long long gap) {
     T* ff = ffbuf(d);
     const LineRange lr{lbeg, lcnt, gap_at, gap};
     if (d == 1) {  // y sweep: z-fastest face-field lines, lr ranges over z
-      dim3 grid((unsigned)((lcnt + RZ_Z - 1) / RZ_Z), (nx + 4 + RZ_X - 1) / RZ_X, 5);
-      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+      const long long lines = lcnt * (nx + 4);
+      const int nseg = segments(1, 5 * lines);
+      dim3 grid((unsigned)((lcnt + RZ_Z - 1) / RZ_Z), (nx + 4 + RZ_X - 1) / RZ_X, 5 * nseg);
+      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
     } else {
-      const int blocks = (int)((5 * lcnt + 127) / 128);
-      if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
-      if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr);
+      const int nseg = segments(d, 5 * lcnt);
+      const int blocks = (int)((5 * lcnt * nseg + 127) / 128);
+      if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
+      if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
     }
     c->total_launches += 1;
   };

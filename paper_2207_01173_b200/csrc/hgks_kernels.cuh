@@ -172,12 +172,14 @@ struct LineRange {
 // fastest axis of the state, so reads and writes are coalesced); the y sweep is recon_yz_kernel.
 template <typename T, int DIR>
 __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
-                                                    const Ctl* __restrict__ ctl, LineRange lr) {
+                                                    const Ctl* __restrict__ ctl, LineRange lr, int nseg) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;
   const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= 5 * lr.lcnt) return;
+  const long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e0 >= 5 * lr.lcnt * nseg) return;
+  const int seg = (int)(e0 / (5 * lr.lcnt));  // segment of the march (outermost: lines stay coalesced)
+  const long long e = e0 - seg * 5 * lr.lcnt;
   const int c = (int)(e / lr.lcnt);
   const long long j = e % lr.lcnt;
   const long long l = lr.lbeg + j + (j >= lr.gap_at ? lr.gap : 0);
@@ -193,14 +195,18 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const T* jfn = g.jf[DIR];
   // every cell's WENO pair is evaluated at the same call site (the loop body), so all faces see
   // bitwise-identical arithmetic (uniform flow stays exactly uniform, O-P1)
-  T s1v = p[0], s2v = p[sN], s3 = p[2 * sN], s4 = p[3 * sN], s5;
-  T Ap = T(0), Bp = T(0);  // edges of cell fn-1
+  // faces [fs, fe) of this segment: the march starts one cell early (cell fs-1, whose right edge is
+  // Q^l of face fs) from the window Qbar_{fs-3..fs}; the cells' WENO pairs are the same bits whatever
+  // the segmentation
   const int nf = L.nf;
-  for (int fn = -1; fn < nf; ++fn) {
+  const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
+  T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
+  T Ap = T(0), Bp = T(0);  // edges of cell fn-1
+  for (int fn = fs - 1; fn < fe; ++fn) {
     s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
-    if (fn >= 0) {
+    if (fn >= fs) {
       const T ih = jfn[fn];  // metric of the face (O-18; 1/h on uniform axes)
       ff[L.at(0, c, fn, l)] = Bp;
       ff[L.at(1, c, fn, l)] = Ac;
@@ -229,11 +235,11 @@ constexpr int RZ_Z = 32, RZ_X = 4;
 // interior z lines run while the z halo is in flight, the 4 ghost-plane z lines after it).
 template <typename T>
 __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restrict__ q, T* __restrict__ ff, Geo<T> g,
-                                                                const Ctl* __restrict__ ctl, LineRange zr) {
+                                                                const Ctl* __restrict__ ctl, LineRange zr, int nseg) {
   if (ctl->halt) return;
   const FFLayout<T, 1> L = ff_layout<T, 1>(g);
   const int tz = threadIdx.x % RZ_Z, tx = threadIdx.x / RZ_Z;
-  const int c = blockIdx.z;
+  const int c = blockIdx.z % 5, seg = blockIdx.z / 5;
   const long long jz = (long long)blockIdx.x * RZ_Z + tz;
   const int x = blockIdx.y * RZ_X + tx - 2;
   if (jz >= zr.lcnt || x >= g.n[0] + 2) return;
@@ -243,14 +249,15 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
   const T* p = q + 3LL * (g.plane + g.px + 1) + (long long)gv * g.vs - 3 * sN + (long long)z * g.plane + x;
   const T* jfn = g.jf[1];
   const long long l = L.line(z, x);
-  T s1v = p[0], s2v = p[sN], s3 = p[2 * sN], s4 = p[3 * sN], s5;
-  T Ap = T(0), Bp = T(0);
   const int nf = L.nf;
-  for (int fn = -1; fn < nf; ++fn) {
+  const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
+  T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
+  T Ap = T(0), Bp = T(0);
+  for (int fn = fs - 1; fn < fe; ++fn) {
     s5 = p[(fn + 5) * sN];
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);
-    if (fn >= 0) {
+    if (fn >= fs) {
       const T ih = jfn[fn];
       ff[L.at(0, c, fn, l)] = Bp;
       ff[L.at(1, c, fn, l)] = Ac;
