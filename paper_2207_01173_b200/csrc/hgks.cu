@@ -435,12 +435,17 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     c->flux_attr_set[STAGE - 1] = true;
   }
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+#ifndef HGKS_DEBUG_SERIAL
+#define HGKS_DEBUG_SERIAL 0  // timing experiment only: reconstruction on the compute stream (no overlap)
+#endif
+  cudaStream_t rs = HGKS_DEBUG_SERIAL ? c->s : c->s2;  // the reconstruction stream
   // Two streams: the reconstruction sweep of the next direction (memory-bound) runs on s2 while the
   // flux sweep of the current one (FP64-bound) runs on s.  Face-field buffer FF[pos & 1] by position
-  // in the sweep order; recon(pos 2) waits for flux(pos 0) before reusing its buffer.  recon(pos 1)
-  // becomes ready together with flux(pos 0) and floods the SMs first, delaying that flux kernel by
-  // about its own duration; recon(pos 2) starts behind flux(pos 1) and costs it little (measured:
-  // the delay follows the position, not the direction -- y, x, z moved it from the x to the y flux).
+  // in the sweep order; recon(pos 2) waits for flux(pos 0) before reusing its buffer.  Measured at
+  // 256^3 (HGKS_DEBUG_SERIAL): the two flux kernels that run beside a reconstruction slow down by that
+  // reconstruction's own serial time, so the overlap is neutral there (285M cell-updates/s either
+  // way) and only pays on thin slabs (256 x 256 x 32: +1 %) -- two blocks per SM already fill the
+  // register file, so a concurrent reconstruction block always displaces flux work.
   // Stage input: x/y ghosts written (ev_xy, recorded by fill_ghosts on c->s); z ghosts land on
   // c->sc (ev_halo).  The first sweep's face lines of the interior z planes need no z ghost, so
   // they run while the halo is in flight; its ghost-plane lines (z = -2, -1, nz, nz+1) and every
@@ -451,7 +456,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   const int order[3] = {HGKS_SWEEP_ORDER ? 1 : 0, HGKS_SWEEP_ORDER ? 0 : 1, 2};
   int pos_of[3];
   for (int k = 0; k < 3; ++k) pos_of[order[k]] = k;
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_xy, 0));
+  CUDA_TRY(c, cudaStreamWaitEvent(rs, c->ev_xy, 0));
   const int n3[3] = {nx, ny, nz};
   auto ffbuf = [&](int d) { return (T*)c->FF[pos_of[d] & 1]; };
   // Each reconstruction thread marches along the normal; on thin slabs (few lines) the march is
@@ -471,19 +476,19 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
       const long long lines = lcnt * (nx + 4);
       const int nseg = segments(1, 5 * lines);
       dim3 grid((unsigned)((lcnt + RZ_Z - 1) / RZ_Z), (nx + 4 + RZ_X - 1) / RZ_X, 5 * nseg);
-      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
+      recon_yz_kernel<T><<<grid, RZ_Z * RZ_X, 0, rs>>>(q, ff, g, c->ctl, lr, nseg);
     } else {
       const int nseg = segments(d, 5 * lcnt);
       const int blocks = (int)((5 * lcnt * nseg + 127) / 128);
-      if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
-      if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, c->s2>>>(q, ff, g, c->ctl, lr, nseg);
+      if (d == 0) recon_kernel<T, 0><<<blocks, 128, 0, rs>>>(q, ff, g, c->ctl, lr, nseg);
+      if (d == 2) recon_kernel<T, 2><<<blocks, 128, 0, rs>>>(q, ff, g, c->ctl, lr, nseg);
     }
     c->total_launches += 1;
   };
   auto recon = [&](int d) -> int {
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
     const long long nl = (long long)ff_pitch(n1, (int)sizeof(T)) * (n2 + 4);
-    prof_begin(c, HGKS_K_RECON, c->s2);
+    prof_begin(c, HGKS_K_RECON, rs);
     if (pos_of[d] == 0) {  // first sweep: interior z lines, then (after the halo) the ghost-plane ones
       if (d == 1) {
         recon_launch(1, 0, nz, nz, 0);
@@ -491,9 +496,9 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
         const long long w0 = ff_pitch(ny, (int)sizeof(T));
         recon_launch(0, 2 * w0, (long long)nz * w0, nl, 0);
       }
-      prof_end(c, HGKS_K_RECON, c->s2);
-      CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_halo, 0));
-      prof_begin(c, HGKS_K_RECON, c->s2);
+      prof_end(c, HGKS_K_RECON, rs);
+      CUDA_TRY(c, cudaStreamWaitEvent(rs, c->ev_halo, 0));
+      prof_begin(c, HGKS_K_RECON, rs);
       if (d == 1) {
         recon_launch(1, -2, 4, 2, nz);
       } else {
@@ -505,8 +510,8 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     } else {
       recon_launch(d, 0, nl, nl, 0);
     }
-    prof_end(c, HGKS_K_RECON, c->s2);
-    CUDA_TRY(c, cudaEventRecord(c->ev_rec[d], c->s2));
+    prof_end(c, HGKS_K_RECON, rs);
+    CUDA_TRY(c, cudaEventRecord(c->ev_rec[d], rs));
     return HGKS_OK;
   };
   auto flux = [&](int d) -> int {
@@ -545,7 +550,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   // enqueue order matters: an event must be recorded before a wait on it is enqueued
   int rc;
   if ((rc = recon(order[0])) || (rc = recon(order[1])) || (rc = flux(order[0]))) return rc;
-  CUDA_TRY(c, cudaStreamWaitEvent(c->s2, c->ev_flux[order[0]], 0));  // its face-field buffer is free again
+  CUDA_TRY(c, cudaStreamWaitEvent(rs, c->ev_flux[order[0]], 0));  // its face-field buffer is free again
   if ((rc = recon(order[2])) || (rc = flux(order[1])) || (rc = flux(order[2]))) return rc;
   c->total_launches += 3;
   CUDA_TRY(c, cudaGetLastError());
