@@ -86,6 +86,9 @@ struct hgks_ctx {
   cudaEvent_t lb_post = nullptr, lb_done = nullptr, lb_rpost = nullptr, lb_rdone = nullptr;
   LoopGroup* grp = nullptr;
   bool flux_attr_set[2] = {false, false};  // max dynamic shared memory set for the stage-1/2 flux kernels
+  bool graphs = true;                       // replay pairs of steps as CUDA graphs (run_steps_graphed)
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // per parity of c->cur
+  long long graph_launches = 0;             // kernels in one replay (launch accounting)
   void* red_tmp = nullptr;            // loopback reduction result before the in-place write-back
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   Ctl* ctl = nullptr;
@@ -418,22 +421,29 @@ static int fill_ghosts(hgks_ctx* c, T* q, bool wait_halo) {
   return HGKS_OK;
 }
 
+// function attributes belong to the device: kept per context (one device each), not process-wide;
+// also set before a graph capture (no attribute calls while capturing)
+template <typename T, int STAGE>
+static int set_flux_attrs(hgks_ctx* c) {
+  if (c->flux_attr_set[STAGE - 1]) return HGKS_OK;
+  const int sm = (int)flux_smem_bytes<T>();
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  c->flux_attr_set[STAGE - 1] = true;
+  return HGKS_OK;
+}
+
 template <typename T, int STAGE>
 static int flux_sweeps(hgks_ctx* c, const T* q) {
   Geo<T> g = make_geo<T>(c);
   GasK<T> gas = make_gas<T>(c->p);
   const size_t smem = flux_smem_bytes<T>();
-  // function attributes belong to the device: kept per context (one device each), not process-wide
-  if (!c->flux_attr_set[STAGE - 1]) {
-    const int sm = (int)smem;
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    c->flux_attr_set[STAGE - 1] = true;
-  }
+  int rc0;
+  if ((rc0 = set_flux_attrs<T, STAGE>(c))) return rc0;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
 #ifndef HGKS_DEBUG_SERIAL
 #define HGKS_DEBUG_SERIAL 0  // timing experiment only: reconstruction on the compute stream (no overlap)
@@ -637,6 +647,41 @@ static int run_steps(hgks_ctx* c, int nsteps) {
   return HGKS_OK;
 }
 
+// CUDA graph of two S2O4 steps (dt/commit, ghosts, halo, 3 reconstruction + 3 flux sweeps and the
+// update of both stages, across the three streams), one per parity of the Q^n / R buffers, replayed
+// for each pair of steps.  Every kernel argument is fixed for the context's lifetime (dt, force and
+// halt live in the device control block), so a graph is captured once.  Single-rank contexts with
+// profiling off only (NCCL and loopback collectives stay on the plain path); HGKS_GRAPHS=0 disables.
+template <typename T>
+static int run_steps_graphed(hgks_ctx* c, int nsteps) {
+  if (!c->graphs || c->prof.on || c->p.nranks != 1 || nsteps < 2) return run_steps<T>(c, nsteps);
+  const int par = c->cur;
+  int rc;
+  if (!c->gexec[par]) {
+    if ((rc = set_flux_attrs<T, 1>(c)) || (rc = set_flux_attrs<T, 2>(c))) return rc;
+    const long long tl = c->total_launches;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
+    rc = run_steps<T>(c, 2);  // enqueues (records) two steps; toggles cur twice
+    const cudaError_t e = cudaStreamEndCapture(c->s, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(c, HGKS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    c->graph_launches = c->total_launches - tl;
+    c->total_launches = tl;
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec[par], graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(c, HGKS_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+  }
+  for (int i = 0; i + 1 < nsteps; i += 2) {
+    CUDA_TRY(c, cudaGraphLaunch(c->gexec[par], c->s));
+    c->total_launches += c->graph_launches;
+  }
+  return (nsteps & 1) ? run_steps<T>(c, 1) : HGKS_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------------------------
@@ -709,6 +754,10 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
 
   hgks_ctx* c = new hgks_ctx();
   c->p = *p;
+  {
+    const char* ge = getenv("HGKS_GRAPHS");
+    c->graphs = !(ge && ge[0] == '0');
+  }
   c->p.nccl_id = nullptr;
   for (int d = 0; d < 3; ++d) {
     c->n[d] = p->n[d];
@@ -962,7 +1011,7 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   const int chunk = t_end > 0.0 ? 16 : (nsteps > 0 ? nsteps : 1);
   for (int done = 0; done < nsteps || done == 0; done += chunk) {
     const int n = std::min(chunk, nsteps - done);
-    int rc = c->fp32 ? run_steps<float>(c, n) : run_steps<double>(c, n);
+    int rc = c->fp32 ? run_steps_graphed<float>(c, n) : run_steps_graphed<double>(c, n);
     if (rc) return rc;
     CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
     CUDA_TRY(c, cudaStreamSynchronize(c->s));
@@ -1058,6 +1107,8 @@ int hgks_destroy(hgks_ctx* c) {
   if (c->grp) c->grp->barrier();
   if (c->s) cudaStreamSynchronize(c->s);
   if (c->sc) cudaStreamSynchronize(c->sc);
+  for (int b = 0; b < 2; ++b)
+    if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
   if (c->comm) ncclCommDestroy(c->comm);
   lb_leave(c);
   cudaFree(c->red_tmp);

@@ -259,6 +259,33 @@ def test_t_end_clamp():
         assert s.t == pytest.approx(0.05, rel=1e-14)
 
 
+@pytest.mark.parametrize("precision", [H.HGKS_FP64, H.HGKS_FP32])
+def test_graph_replay_bitwise(precision, monkeypatch):
+    """Pairs of steps replayed as CUDA graphs (default) against the plain launch path (HGKS_GRAPHS=0):
+    identical bits for odd and even step counts, both buffer parities and the chunked t_end path."""
+    q, dx = inputs.perturbed((20, 18, 12), seed=9, amp=0.08)
+
+    def run(env):
+        if env is None:
+            monkeypatch.delenv("HGKS_GRAPHS", raising=False)
+        else:
+            monkeypatch.setenv("HGKS_GRAPHS", env)
+        with _solver((20, 18, 12), (0.0,) * 3, (2 * math.pi,) * 3, mu=2e-3, cfl=0.4, precision=precision) as s:
+            s.set_state(q)
+            out = []
+            for n in (2, 5, 1, 4):  # parities 0, 0 -> 1, 1 -> 0, 0
+                s.step(n)
+                out.append(s.get_state())
+            s.step(1_000_000, t_end=s.t + 0.2)
+            out.append(s.get_state())
+            return out, s.t
+    g, tg = run(None)
+    p, tp = run("0")
+    assert tg == tp
+    for a, b in zip(g, p):
+        assert np.array_equal(a, b)
+
+
 def test_t_end_many_steps_chunked():
     """hgks_step with a t_end enqueues in chunks and stops at the halt: a huge nsteps costs nothing,
     and splitting the call anywhere gives the same bits (same dt sequence, same commits)."""
