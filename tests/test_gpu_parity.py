@@ -286,6 +286,33 @@ def test_graph_replay_bitwise(precision, monkeypatch):
         assert np.array_equal(a, b)
 
 
+def _gpu_wave_error(n, T=0.2):
+    """3-D diagonal density wave (k = (1,1,1), U = (1,1,1), tau = 0) advected to T on the GPU; L1
+    error of rho against the exact cell averages (4-point Gauss-Legendre per axis)."""
+    q, h = inputs.density_wave(n, k=(1, 1, 1), vel=(1.0, 1.0, 1.0))
+    steps = int(math.ceil(T / (0.1 * h[0])))
+    with _solver((n, n, n), (0.0,) * 3, (2.0,) * 3, mu=0.0, dt_fixed=T / steps) as s:
+        s.set_state(q)
+        s.step(steps)
+        got = s.get_state()[0]
+    gx, gw = np.polynomial.legendre.leggauss(4)
+    xc = inputs.cell_centres(n, 0.0, 2.0)
+    ex = np.zeros((n, n, n))
+    for a, wa in zip(gx, gw):
+        for b, wb in zip(gx, gw):
+            for c, wc in zip(gx, gw):
+                Z, Y, X = np.meshgrid(xc + 0.5 * h[2] * c, xc + 0.5 * h[1] * b, xc + 0.5 * h[0] * a, indexing="ij")
+                ex += wa * wb * wc / 8 * (1 + 0.2 * np.sin(math.pi * ((X - T) + (Y - T) + (Z - T))))
+    return np.abs(got - ex).mean()
+
+
+def test_fifth_order_convergence_3d_wave_gpu():
+    """O-P4 on the GPU path in 3-D (every sweep, both tangential Gauss abscissae): L1 order >= 4.5."""
+    errs = [_gpu_wave_error(n) for n in (16, 32, 64)]
+    orders = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
+    assert min(orders) >= 4.5, (errs, orders)
+
+
 def test_t_end_many_steps_chunked():
     """hgks_step with a t_end enqueues in chunks and stops at the halt: a huge nsteps costs nothing,
     and splitting the call anywhere gives the same bits (same dt sequence, same commits)."""
