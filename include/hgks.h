@@ -90,7 +90,7 @@ typedef struct {
   int64_t group_key;     /* nranks > 1 without NCCL: != 0 joins the in-process LOOPBACK group of
                             that key (nccl_id must be NULL).  The nranks contexts of the group live
                             in ONE process, each driven by its own host thread, and may share one
-                            device: halos move by device-to-device copies ordered with CUDA events,
+                            device (ranks on different devices get peer access enabled): halos move by device-to-device copies ordered with CUDA events,
                             reductions run in a fixed rank order on the device, and the collective
                             calls synchronise the threads with a host barrier (120 s timeout ->
                             HGKS_ENCCL).  Same kernels, slab split and halo plan as the NCCL path:

@@ -375,6 +375,19 @@ static int lb_join(hgks_ctx* c) {
     G->refs += 1;
     c->grp = G;
   }
+  int rc = lb_barrier(c);
+  if (rc) return rc;
+  // ranks on different devices read each other's buffers (halo copies, reduction kernel): peer access
+  for (int q = 0; q < c->p.nranks; ++q) {
+    const int d = G->m[q]->dev;
+    if (d == c->dev) continue;
+    int can = 0;
+    CUDA_TRY(c, cudaDeviceCanAccessPeer(&can, c->dev, d));
+    if (!can) return fail(c, HGKS_ECUDA, "loopback group: device %d cannot access peer device %d", c->dev, d);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(c, HGKS_ECUDA, "peer access: %s", cudaGetErrorString(e));
+    cudaGetLastError();  // clear a sticky "already enabled"
+  }
   return lb_barrier(c);
 }
 
