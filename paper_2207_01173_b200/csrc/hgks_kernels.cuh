@@ -1,12 +1,16 @@
 // hgks_kernels.cuh — sm_100a kernels of one S2O4 stage (product path).
 //
-//   flux_kernel<T, DIR, STAGE>  fused: normal WENO reconstruction of a tile of face lines into
-//                               shared memory (A2) -> tangential pass t1 (A3) -> per-Gauss-point
-//                               thread: tangential pass t2 + BGK flux (A4-A6) -> 4-point face
-//                               quadrature by warp shuffles (A7) -> face-flux array
+//   recon_kernel<T, 0/2>,       normal reconstruction (A2): one thread per (face line, component,
+//   recon_yz_kernel<T>          march segment), WENO5-Z edges once per cell, six face fields per face
+//                               written to the face-field array of the sweep
+//   flux_kernel<T, DIR, STAGE>  fused per tile of 8x8 faces, marching up to 16 normal faces: 16-byte
+//                               cp.async copy of the face fields (A) -> tangential pass t1 (B, A3) ->
+//                               per-Gauss-point thread: tangential pass t2 + BGK flux (C, A4-A6) ->
+//                               4-point face quadrature by warp shuffles (A7) -> face-flux array
 //   update_kernel<T, STAGE>     flux divergence L, d_t L (Eqs. (3)-(4)) + Eq. (7) stage update,
 //                               stage-2 epilogue: validity flags + CFL wave-speed max (A0, A8)
-//   ghost_xy_kernel<T>          periodic ghost layers along x and y (A1, O-16)
+//   ghost_wall_kernel<T>,       isothermal-wall mirror ghosts (O-17) and periodic x/y ghost bands
+//   ghost_xy_kernel<T>          (A1, O-16); the z halo is a copy / NCCL / loopback exchange (hgks.cu)
 //   cfl_kernel<T> / dt_kernel   initial wave-speed max, per-step dt + commit logic (A0)
 //
 // Layout of a ghosted state (elements of T): [nz_l+6][5][ny+6][nx+6], x fastest.
