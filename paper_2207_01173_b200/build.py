@@ -29,7 +29,7 @@ def sources():
                   + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(), extra=()) -> str:
     srcs = sources()
     out = out or LIB
     if os.sep not in out:  # bare file name: a variant next to the default library
@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     inc, nccl_so, nccl_dir = _nccl_dirs()
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           *["-D" + d for d in defines], "-I", INCLUDE, "-I", inc, "-o", out, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
+           *["-D" + d for d in defines], *extra, "-I", INCLUDE, "-I", inc, "-o", out, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
            "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir] + (["-rdc=false"] if False else [])
     subprocess.check_call(cmd)
     return out
@@ -48,4 +48,5 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[5:] for a in sys.argv[1:] if a.startswith("-out=")]
-    print(build(force=True, verbose="-v" in sys.argv, out=outs[0] if outs else None, defines=defs))
+    extra = [a[4:] for a in sys.argv[1:] if a.startswith("-nv=")]  # raw nvcc flags, e.g. -nv=-use_fast_math
+    print(build(force=True, verbose="-v" in sys.argv, out=outs[0] if outs else None, defines=defs, extra=extra))
