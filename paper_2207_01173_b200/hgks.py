@@ -8,6 +8,11 @@ Names mirror the C ABI: hgks_create, hgks_local_extent, hgks_set_state, hgks_ste
 hgks_get_state, hgks_destroy, hgks_last_error, plus a small ``Solver`` convenience wrapper.
 States use the ABI layout [5][nz_local][ny][nx] float64 (numpy host arrays, or torch CUDA
 tensors passed by device pointer).
+
+Multi-rank: one process per GPU with an NCCL unique id (``hgks_get_nccl_id`` on rank 0, broadcast,
+``make_params(..., rank, nranks, nccl_id=...)``), or the in-process loopback group for tests on one
+device (``run_loopback_group`` with ``group_key``).  Environment: ``HGKS_GRAPHS=0`` disables the
+CUDA-graph replay of step pairs (single-rank contexts); ``HGKS_LIB`` points at another build.
 """
 from __future__ import annotations
 
