@@ -2,10 +2,21 @@
 """bench.py — HGKS S2O4 step throughput on B200 (BASELINE.json metric: cell-updates/s, TGV 256^3).
 
 One "step" = one full two-stage S2O4 step (A0..A8 of SURVEY.md §8(a)) over the whole grid.
-Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under torch.distributed.run
-(one rank per GPU, NCCL halos along z).  --impl reference times the plain CPU oracle instead.
 
-Prints ONE JSON line on rank 0.
+Launch modes (one JSON line from rank 0 in every mode):
+  python bench.py                          1 GPU (N = 1)
+  torchrun --nproc-per-node N bench.py --gpus N
+                                           N ranks, one per GPU, NCCL z-slab halos (the driver's launch)
+  python bench.py --gpus N                 same: re-executes itself under torch.distributed.run when
+                                           WORLD_SIZE is unset (needs N visible GPUs)
+  python bench.py --gpus N --transport loopback
+                                           N slab ranks in ONE process on host threads, sharing the
+                                           visible GPUs round-robin (the in-process loopback group of
+                                           hgks.h: same kernels, slab split, halo plan and collectives'
+                                           placement as NCCL) -- a dry run of the N-rank path on 1 GPU
+  python bench.py --impl reference         the plain CPU oracle on the host cores (reference arm)
+
+Prints ONE JSON line on rank 0 (DESIGN.md §8 "Measurement").
 """
 from __future__ import annotations
 
@@ -13,6 +24,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -24,17 +36,34 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "cell-updates/s"
-# FP64 peak of B200 derived from unit counts: 148 SMs x 64 FP64 FMA/clk
-# x 2 flop x clocks.max.sm (1965 MHz, MEASURED_PEAKS.json sm_max_mhz)
-N_SM, FP64_FMA_PER_CLK = 148, 64
+N_SM = 148
+# derived nominal ALU peaks (per SM per clock): 64 FP64 FMA, 128 FP32 FMA
+FP64_FMA_PER_CLK, FP32_FMA_PER_CLK = 64, 128
+
+
+def _json(path):
+    try:
+        with open(os.path.join(ROOT, path)) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
-    except Exception:
-        return {}
+    return _json("MEASURED_PEAKS.json") or {}
+
+
+def alu_peak(kind: str, sm_max: float):
+    """(TFLOP/s, source) of the FP64 (kind 'dfma') or FP32 ('ffma') FMA pipe: the committed
+    microbenchmark measurement (profiles/alu_peaks.json, tools/microbench/alu_peaks.cu) when
+    present, else derived from unit counts x clocks.max.sm."""
+    per_clk = FP64_FMA_PER_CLK if kind == "dfma" else FP32_FMA_PER_CLK
+    derived = N_SM * per_clk * 2 * sm_max * 1e6 / 1e12
+    m = _json(os.path.join("profiles", "alu_peaks.json"))
+    if m and m.get(kind + "_tflops"):
+        return float(m[kind + "_tflops"]), (f"of measured: {kind.upper()} microbenchmark {m[kind + '_tflops']:.2f} TF "
+                                            f"(profiles/alu_peaks.json; derived nominal {derived:.2f})")
+    return derived, f"of derived nominal: {N_SM} SMs x {per_clk} FMA/clk x 2 x {sm_max:.0f} MHz"
 
 
 class ClockSampler:
@@ -89,34 +118,67 @@ def _dist():
     return ws, rank, local
 
 
-def _flop_table():
-    path = os.path.join(ROOT, "profiles", "flux_flops.json")
-    try:
-        with open(path) as f:
-            return json.load(f)
-    except Exception:
-        return None
-
-
-def cpu_baseline(n: int, planes: int, mu: float, dx, stage_count: int = 2):
-    """Oracle (CPU, all host cores via OpenMP) on a bounded sample of the same TGV workload:
-    the operator L, d_t L of `planes` z-planes of the n^3 field (true neighbour ghosts), once
-    per stage.  Returns (cell-updates/s, cores, seconds, sample description)."""
-    from oracle import oracle as O
+# ---------------------------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands (test infrastructure; only this leg and --impl reference
+# execute it)
+# ---------------------------------------------------------------------------------------------
+def _tgv_block(n: int, planes: int):
     from paper_2207_01173_b200 import inputs
-    # ghosted block: z planes -3 .. planes+2 of the periodic n^3 field, x/y ghosts by wrap
     zidx = np.arange(-3, planes + 3) % n
     blk_z = np.concatenate([inputs.tgv(n, z_begin=int(z), nz_local=1)[0] for z in zidx], axis=1)
     w = np.arange(-3, n + 3) % n
-    blk = np.ascontiguousarray(blk_z[:, :, w][:, :, :, w])
+    return np.ascontiguousarray(blk_z[:, :, w][:, :, :, w])
+
+
+def cpu_operator_sample(n: int, planes: int, mu: float, threads: int = 0, stage_count: int = 2):
+    """Oracle operator L, d_t L on `planes` z-planes of the TGV n^3 field (true neighbour ghosts),
+    once per stage = the flux work of one S2O4 step on n*n*planes cells.  Returns
+    (cell-updates/s, cores used, seconds, sample description)."""
+    from oracle import oracle as O
+    blk = _tgv_block(n, planes)
     gas = O.make_gas(mu=mu)
     dummy = np.zeros((5, planes, n, n))
-    t0 = time.perf_counter()
-    for _ in range(stage_count):
-        O.operator(gas, dummy, dx, 1e-3, qg=blk)
-    sec = time.perf_counter() - t0
-    cells = n * n * planes
-    return cells / sec, O.num_threads(), sec, f"oracle operator on {n}x{n}x{planes} z-planes of TGV {n}^3, x{stage_count} stages"
+    O.set_num_threads(threads)
+    try:
+        cores = O.num_threads()
+        t0 = time.perf_counter()
+        for _ in range(stage_count):
+            O.operator(gas, dummy, (2 * math.pi / n,) * 3, 1e-3, qg=blk)
+        sec = time.perf_counter() - t0
+    finally:
+        O.set_num_threads(0)
+    return n * n * planes / sec, cores, sec, f"oracle operator on {n}x{n}x{planes} z-planes of TGV {n}^3, x{stage_count} stages"
+
+
+def cpu_run_c1(threads: int = 0, steps: int = 10):
+    """BASELINE config 1 in full: TGV 32^3, `steps` complete CFL S2O4 steps of the oracle."""
+    from oracle import oracle as O
+    from paper_2207_01173_b200 import inputs
+    n = 32
+    q, dx = inputs.tgv(n)
+    gas = O.make_gas(mu=inputs.tgv_params()["mu"])
+    O.set_num_threads(threads)
+    try:
+        cores = O.num_threads()
+        t0 = time.perf_counter()
+        O.run(gas, q, dx, steps)
+        sec = time.perf_counter() - t0
+    finally:
+        O.set_num_threads(0)
+    return n ** 3 * steps / sec, cores, sec
+
+
+def cpu_baseline_block(n: int, planes: int, mu: float):
+    v, cores, sec, sample = cpu_operator_sample(n, planes, mu)
+    v1, _, sec1, _ = cpu_operator_sample(n, 1, mu, threads=1)
+    c1, c1_cores, c1_sec = cpu_run_c1()
+    c1s, _, c1s_sec = cpu_run_c1(threads=1, steps=2)
+    return {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "seconds": sec,
+            "single_thread": {"value": v1, "cores": 1, "sample": f"oracle operator on {n}x{n}x1 z-plane, x2 stages",
+                              "seconds": sec1},
+            "c1_tgv32_10steps": {"value": c1, "cores": c1_cores, "seconds": c1_sec,
+                                 "single_thread_value": c1s, "single_thread_sample": "2 steps", "single_thread_seconds": c1s_sec}}
 
 
 def run_reference(args):
@@ -124,12 +186,12 @@ def run_reference(args):
     if rank != 0:
         return
     n = args.n
-    prm = __import__("paper_2207_01173_b200.inputs", fromlist=["tgv_params"]).tgv_params()
-    dx = (2 * math.pi / n,) * 3
+    from paper_2207_01173_b200 import inputs
+    prm = inputs.tgv_params()
     planes = 1
-    times = []
+    times, cores, sample = [], None, ""
     for i in range(args.warmup + args.steps):
-        v, cores, sec, sample = cpu_baseline(n, planes, prm["mu"], dx)
+        _, cores, sec, sample = cpu_operator_sample(n, planes, prm["mu"])
         if i >= args.warmup:
             times.append(sec)
     ms = 1000 * float(np.mean(times))
@@ -144,36 +206,92 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="hgks", choices=["hgks", "reference"])
-    ap.add_argument("--n", type=int, default=256, help="TGV grid n^3 (BASELINE config 3: 256)")
-    ap.add_argument("--workload", default="tgv", choices=["tgv", "channel"],
-                    help="tgv: config 3 (headline); channel: config 4 (H2 128x256x128 unless --channel-grid)")
-    ap.add_argument("--channel-grid", default="128,256,128")
-    ap.add_argument("--weak", action="store_true", help="weak scaling: n x n x (n/8 * N) per job")
-    ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--only-fp32", action="store_true", help="profiling aid: run only the fp32 leg")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-planes", type=int, default=4)
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+# ---------------------------------------------------------------------------------------------
+# rank environments: NCCL (one process per GPU) or the in-process loopback group (host threads)
+# ---------------------------------------------------------------------------------------------
+class NcclEnv:
+    transport = "nccl"
 
+    def __init__(self, dist, ws, rank, local):
+        import torch
+        self.dist, self.ws, self.rank, self.device = dist, ws, rank, local
+        self.stream = torch.cuda.Stream(device=local)
+
+    def barrier(self):
+        import torch
+        if self.ws > 1:
+            self.dist.barrier()
+        torch.cuda.synchronize(self.device)
+
+    def reduce(self, x: float, op: str) -> float:
+        if self.ws == 1:
+            return x
+        import torch
+        t = torch.tensor([x], device=f"cuda:{self.device}", dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def comm_kwargs(self):
+        """A FRESH NCCL unique id for every context (NCCL's bootstrap root serves one init)."""
+        if self.ws == 1:
+            return {}
+        from paper_2207_01173_b200 import hgks as H
+        obj = [H.hgks_get_nccl_id() if self.rank == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0)
+        return {"nccl_id": obj[0]}
+
+
+class LoopbackShared:
+    def __init__(self, ws):
+        self.ws = ws
+        self.bar = threading.Barrier(ws)
+        self.vals = [0.0] * ws
+        self.keys = iter(range(os.getpid() * 1000 + 1, os.getpid() * 1000 + 1000))
+        self.key = None
+
+
+class LoopbackEnv:
+    transport = "loopback"
+
+    def __init__(self, shared: LoopbackShared, rank: int, ndev: int):
+        import torch
+        self.sh, self.ws, self.rank = shared, shared.ws, rank
+        self.device = rank % ndev
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.Stream(device=self.device)
+
+    def barrier(self):
+        import torch
+        self.sh.bar.wait()
+        torch.cuda.synchronize(self.device)
+        self.sh.bar.wait()
+
+    def reduce(self, x: float, op: str) -> float:
+        self.sh.vals[self.rank] = x
+        self.sh.bar.wait()
+        v = max(self.sh.vals) if op == "max" else sum(self.sh.vals)
+        self.sh.bar.wait()
+        return v
+
+    def comm_kwargs(self):
+        if self.rank == 0:
+            self.sh.key = next(self.sh.keys)
+        self.sh.bar.wait()
+        key = self.sh.key
+        self.sh.bar.wait()
+        return {"group_key": key}
+
+
+# ---------------------------------------------------------------------------------------------
+# one rank's measurement (fp64 and fp32 legs)
+# ---------------------------------------------------------------------------------------------
+def measure_rank(args, env) -> dict | None:
     import torch
-    import torch.distributed as dist
 
     from paper_2207_01173_b200 import hgks as H
     from paper_2207_01173_b200 import inputs
 
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ws, rank = env.ws, env.rank
     n = args.n
     nz = (n // 8) * ws if args.weak else n
     grid = (n, n, nz)
@@ -182,71 +300,50 @@ def main():
     if channel:
         grid = tuple(int(x) for x in args.channel_grid.split(","))
         chp = inputs.channel_params()
-    nccl_id = None
-    if ws > 1:
-        obj = [H.hgks_get_nccl_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    stream = torch.cuda.current_stream()
-
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
+    stream = env.stream
     lo, hi = (-math.pi,) * 3, (math.pi,) * 3  # weak mode: same box, nz = n/8 * N planes (anisotropic dz)
 
     def make_solver(precision):
+        kw = dict(cfl=0.4, precision=precision, rank=rank, nranks=ws, device=env.device,
+                  stream=stream.cuda_stream, **env.comm_kwargs())
         if channel:  # config 4: walls in y, tanh mesh, power-law mu, Pr = 0.7
             return H.Solver(grid, chp["lo"], chp["hi"], mu=chp["mu_w"], mu_law=H.HGKS_MU_POWER, T_ref=chp["T_w"],
                             omega=chp["omega"], prandtl=chp["prandtl"], T_wall=chp["T_w"],
                             bc=(H.HGKS_PERIODIC, H.HGKS_WALL_ISOTHERMAL, H.HGKS_PERIODIC),
                             stretch=(H.HGKS_UNIFORM, H.HGKS_TANH, H.HGKS_UNIFORM), stretch_b=(0.0, chp["b_g"], 0.0),
-                            cfl=0.4, precision=precision, rank=rank, nranks=ws, device=local, nccl_id=nccl_id,
-                            stream=stream.cuda_stream,
                             # constant bulk momentum rho_b U_b = 1 (units of the channel, O-27)
-                            force_mode=H.HGKS_FORCE_BULK, force=0.0, force_target=1.0)
-        return H.Solver(grid, lo, hi, mu=prm["mu"], cfl=0.4, precision=precision, rank=rank, nranks=ws,
-                        device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+                            force_mode=H.HGKS_FORCE_BULK, force=0.0, force_target=1.0, **kw)
+        return H.Solver(grid, lo, hi, mu=prm["mu"], **kw)
 
     def local_field(s):
         if channel:
             return inputs.channel(grid, z_begin=s.z0, nz_local=s.nz_local)[0]
-        # TGV on [-pi, pi]^3 with this rank's z planes
-        q, _ = inputs.tgv(grid, z_begin=s.z0, nz_local=s.nz_local)
-        return q
+        return inputs.tgv(grid, z_begin=s.z0, nz_local=s.nz_local)[0]
 
     results = {}
     for prec_name, prec in (("fp64", H.HGKS_FP64), ("fp32", H.HGKS_FP32)):
-        if prec_name == "fp32" and args.no_fp32:
-            continue
-        if prec_name == "fp64" and args.only_fp32:
+        if (prec_name == "fp32" and args.no_fp32) or (prec_name == "fp64" and args.only_fp32):
             continue
         s = make_solver(prec)
         q = local_field(s)
-        qd = torch.from_numpy(q).cuda()
+        with torch.cuda.device(env.device):
+            qd = torch.from_numpy(q).cuda()
         s.set_state(qd)
         s.step(args.warmup)
-        barrier()
+        env.barrier()
         H.hgks_profile_enable(s.ctx, True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
-            barrier()
+        with ClockSampler(env.device) as clk:
+            env.barrier()
             ev0.record(stream)
             s.step(args.steps)
             ev1.record(stream)
-            barrier()
+            env.barrier()
         ms_local = ev0.elapsed_time(ev1)
         ms_k, launches, total_launches = H.hgks_profile_read(s.ctx)
         H.hgks_profile_enable(s.ctx, False)
-        ms = max_over_ranks(ms_local)
+        ms = env.reduce(ms_local, "max")
+        total_launches = int(env.reduce(float(total_launches), "sum"))
         cells = grid[0] * grid[1] * grid[2]
         rate = cells * args.steps / (ms / 1000.0)
         res = dict(ms_per_step=ms / args.steps, value=rate, clocks=clk.summary(), ms_k=ms_k, launches=launches,
@@ -261,14 +358,14 @@ def main():
             for _ in range(3):
                 fn()
             a1.record(stream)
-            torch.cuda.synchronize()
+            torch.cuda.synchronize(env.device)
             aux[name + "_ms"] = a0.elapsed_time(a1) / 3
         res["aux"] = aux
         # e2e through the public API with host buffers (pinned): H2D state, step, D2H state per step
         if not args.no_e2e:
             qh = torch.from_numpy(q).pin_memory()
             qo = torch.empty_like(qh).pin_memory()
-            barrier()
+            env.barrier()
             t0 = time.perf_counter()
             e_ev0, e_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e_ev0.record(stream)
@@ -278,76 +375,166 @@ def main():
                 s.step(1)
                 s.get_state(qo.numpy())
             e_ev1.record(stream)
-            barrier()
-            e_ms = max_over_ranks(e_ev0.elapsed_time(e_ev1))
+            env.barrier()
+            e_ms = env.reduce(e_ev0.elapsed_time(e_ev1), "max")
             res["e2e"] = {"value": cells * e_steps / (e_ms / 1000.0), "unit": "cell-updates/s",
-                          "h2d_bytes_per_step": int(q.nbytes) * ws, "d2h_bytes_per_step": int(q.nbytes) * ws,
+                          "h2d_bytes_per_step": int(env.reduce(float(q.nbytes), "sum")),
+                          "d2h_bytes_per_step": int(env.reduce(float(q.nbytes), "sum")),
                           "steps": e_steps, "wall_s": time.perf_counter() - t0}
         s.close()
         del qd
         torch.cuda.empty_cache()
         results[prec_name] = res
-
     if rank != 0 or args.only_fp32:
-        if ws > 1:
-            dist.destroy_process_group()
-        return
+        return None
+    return {"results": results, "grid": grid, "channel": channel, "prm": prm}
+
+
+def flux_roofline(r, grid, ws, steps, prec: str, sm_max: float):
+    """roofline of the dominant kernel (the fused flux sweeps): executed FP64/FP32 flops per launch
+    (ncu SASS counts per face, profiles/flux_flops.json) / the live CUDA-event launch time."""
+    flux_ms = sum(r["ms_k"][k] for k in ("flux_x", "flux_y", "flux_z"))
+    flux_launches = sum(r["launches"][k] for k in ("flux_x", "flux_y", "flux_z"))
+    kind = "dfma" if prec == "fp64" else "ffma"
+    peak, src = alu_peak(kind, sm_max)
+    roof = {"bound": "alu", "kernel": f"flux_kernel<{'double' if prec == 'fp64' else 'float'},DIR,STAGE> (x,y,z faces, both stages)",
+            "peak": peak, "unit": "TFLOP/s", "peak_source": src,
+            "flux_share_of_step": flux_ms / (r["ms_per_step"] * steps) if r["ms_per_step"] else None,
+            "avg_launch_ms": flux_ms / flux_launches if flux_launches else None, "traffic": None}
+    ftab = _json(os.path.join("profiles", "flux_flops.json"))
+    key1, key2 = f"{prec}_flop_per_face_stage1", f"{prec}_flop_per_face_stage2"
+    if ftab and key1 in ftab:
+        gx, gy, gzl = grid[0], grid[1], grid[2] // ws
+        faces = 3 * gx * gy * gzl + gy * gzl + gx * gzl + gx * gy  # x, y, z faces of one rank's slab
+        flops_step = faces * (ftab[key1] + ftab[key2])
+        achieved = flops_step * steps / (flux_ms / 1000.0) / 1e12
+        roof.update(achieved=achieved, frac=achieved / peak,
+                    flop_count="executed FP%s flops of the flux kernels (SASS: 2 x FMA + MUL + ADD, ncu), %.0f + %.0f per face "
+                               "(stages 1 + 2); the method's own algebra costs more (DESIGN.md §8)" % (prec[2:], ftab[key1], ftab[key2]),
+                    flop_source=ftab.get("source"), traffic=ftab.get(f"{prec}_dram_bytes_per_launch_stage1"),
+                    traffic_note="ncu dram__bytes_read+write per stage-1 flux launch (same counters file)")
+    return roof
+
+
+def report(args, out, ws, transport):
+    results, grid, channel, prm = out["results"], out["grid"], out["channel"], out["prm"]
+    n = args.n
     r64 = results["fp64"]
-    flux_ms = sum(r64["ms_k"][k] for k in ("flux_x", "flux_y", "flux_z"))
-    flux_launches = sum(r64["launches"][k] for k in ("flux_x", "flux_y", "flux_z"))
-    ftab = _flop_table()
-    clk = r64["clocks"]
     peaks = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_tflops = N_SM * FP64_FMA_PER_CLK * 2 * sm_max * 1e6 / 1e12
-    cells_local = grid[0] * grid[1] * grid[2] // ws
-    roof = {"bound": "alu", "kernel": "flux_kernel<double,DIR,STAGE> (x,y,z faces, both stages)",
-            "peak": peak_tflops, "unit": "TFLOP/s",
-            "peak_source": f"derived: {N_SM} SMs x {FP64_FMA_PER_CLK} FP64 FMA/clk x 2 x {sm_max:.0f} MHz (DESIGN.md)",
-            # share of the step's wall time (the reconstruction kernels overlap on a second stream, so
-            # the per-class event sums exceed the wall time; compare with the serialised ncu share)
-            "flux_share_of_step": flux_ms / (r64["ms_per_step"] * args.steps) if r64["ms_per_step"] else None,
-            "avg_launch_ms": flux_ms / flux_launches if flux_launches else None, "traffic": None}
-    if ftab:
-        # executed FP64 flops per face per stage (ncu SASS count, profiles/flux_flops.json)
-        gx, gy, gzl = grid[0], grid[1], grid[2] // ws
-        faces = 3 * cells_local + gy * gzl + gx * gzl + gx * gy  # x, y, z faces of one rank's slab
-        flops_step = faces * (ftab["flop_per_face_stage1"] + ftab["flop_per_face_stage2"])
-        achieved = flops_step * args.steps / (flux_ms / 1000.0) / 1e12
-        roof.update(achieved=achieved, frac=achieved / peak_tflops, flop_source=ftab.get("source"),
-                    traffic=ftab.get("dram_bytes_per_launch"))
-    hbm = float(peaks.get("hbm_gbs", 6542.4))
+    hbm = float(peaks.get("hbm_gbs", 6548.5))
     alg_bytes = 240.0  # fp64 bytes per cell-update (SURVEY §8(d))
+    workload = ("channel_" + "x".join(map(str, grid))) if channel else (f"tgv{n}" + ("_weak" if args.weak else ""))
     line = {
         "metric": METRIC, "value": r64["value"], "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r64["ms_per_step"], "higher_is_better": True,
         "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": ("channel_" + "x".join(map(str, grid))) if channel else (f"tgv{n}" + ("_weak" if args.weak else "")),
-                   "grid": list(grid), "precision": "fp64",
+        "config": {"workload": workload, "grid": list(grid), "precision": "fp64",
                    "mode": "cfl 0.4 (dt allreduce each step)" + (", bulk-momentum forcing (O-27)" if channel else ""),
-                   "decomposition": f"z-slab x{ws}",
+                   "decomposition": f"z-slab x{ws}", "transport": transport,
                    "l2": "inputs larger than L2 (one state = %d MB)" % (5 * grid[0] * grid[1] * grid[2] * 8 // 2**20)},
-        "clocks": clk,
+        "clocks": r64["clocks"],
         "gpu_launches": int(r64["total_launches"]),
-        "roofline": roof,
+        "roofline": flux_roofline(r64, grid, ws, args.steps, "fp64", sm_max),
         "hbm_roofline": {"alg_bytes_per_cell_update": alg_bytes,
                          "achieved_gbs": r64["value"] / ws * alg_bytes / 1e9, "peak_gbs": hbm,
-                         "frac": r64["value"] / ws * alg_bytes / 1e9 / hbm},
+                         "frac": r64["value"] / ws * alg_bytes / 1e9 / hbm, "peak_source": "of measured (MEASURED_PEAKS.json hbm_gbs)"},
         "kernel_ms_per_step": {k: v / args.steps for k, v in r64["ms_k"].items()},
         "aux_ms": r64.get("aux"),
     }
+    if transport == "loopback":
+        line["config"]["note"] = (f"{ws} slab ranks in one process (loopback group) on "
+                                  f"{min(ws, _ndev())} GPU(s): a functional dry run of the N-rank path, not a scaling number")
     if "e2e" in r64:
         line["e2e"] = r64["e2e"]
     if "fp32" in results:
         r32 = results["fp32"]
         line["fp32"] = {"value": r32["value"], "ms_per_step": r32["ms_per_step"], "clocks": r32["clocks"],
                         "e2e": r32.get("e2e"), "speedup_vs_fp64": r32["value"] / r64["value"],
+                        "roofline": flux_roofline(r32, grid, ws, args.steps, "fp32", sm_max),
                         "kernel_ms_per_step": {k: v / args.steps for k, v in r32["ms_k"].items()}}
     if not args.no_cpu and not channel:
-        v, cores, sec, sample = cpu_baseline(n, args.cpu_planes, prm["mu"], (2 * math.pi / n,) * 3)
-        line["cpu_baseline"] = {"value": v, "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
-                                "sample": sample, "seconds": sec}
+        line["cpu_baseline"] = cpu_baseline_block(n, args.cpu_planes, prm["mu"])
     print(json.dumps(line), flush=True)
+
+
+def _ndev():
+    import torch
+    return max(1, torch.cuda.device_count())
+
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hgks", choices=["hgks", "reference"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "loopback"],
+                    help="nccl: one process per GPU; loopback: N ranks in this process (one GPU suffices)")
+    ap.add_argument("--n", type=int, default=256, help="TGV grid n^3 (BASELINE config 3: 256)")
+    ap.add_argument("--workload", default="tgv", choices=["tgv", "channel"],
+                    help="tgv: config 3 (headline); channel: config 4 (H2 128x256x128 unless --channel-grid)")
+    ap.add_argument("--channel-grid", default="128,256,128")
+    ap.add_argument("--weak", action="store_true", help="weak scaling (config 5 with --n 512): n x n x (n/8 * N)")
+    ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--only-fp32", action="store_true", help="profiling aid: run only the fp32 leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-planes", type=int, default=4)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    if args.transport == "nccl" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # the driver launches N > 1 under torch.distributed.run; a bare `--gpus N` re-executes so
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+
+    import torch
+
+    if args.transport == "loopback":
+        ws = args.gpus
+        shared = LoopbackShared(ws)
+        outs, errs = [None] * ws, []
+
+        def work(r):
+            try:
+                outs[r] = measure_rank(args, LoopbackEnv(shared, r, _ndev()))
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                shared.bar.abort()
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(ws)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        if outs[0] is not None:
+            report(args, outs[0], ws, "loopback")
+        return
+
+    import torch.distributed as dist
+    ws, rank, local = _dist()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if ws > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {ws} NCCL ranks need {ws} GPUs, {torch.cuda.device_count()} visible "
+                         "(use --transport loopback for a one-GPU dry run)")
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    out = measure_rank(args, NcclEnv(dist, ws, rank, local))
+    if out is not None:
+        report(args, out, ws, "nccl" if ws > 1 else "none (1 rank)")
     if ws > 1:
         dist.destroy_process_group()
 

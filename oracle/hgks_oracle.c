@@ -27,6 +27,17 @@ int or_num_threads(void) {
 #endif
 }
 
+/* host threading only (bench.py's single-thread / all-core cpu_baseline): n <= 0 restores all cores */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+  static int all = 0;
+  if (all == 0) all = omp_get_max_threads();
+  omp_set_num_threads(n > 0 ? n : all);
+#else
+  (void)n;
+#endif
+}
+
 /* ------------------------------------------------------------------------------------------
  * A.1 gas model.  K = (5 - 3 gamma)/(gamma - 1)  (O-20: evaluated in fp64 as written)
  * ---------------------------------------------------------------------------------------- */

@@ -172,6 +172,7 @@ enum { OR_DIAG_EK = 0, OR_DIAG_ENSTROPHY, OR_DIAG_EPS_S, OR_DIAG_EPS_D, OR_DIAG_
 void or_diagnostics(const or_gas* g, const or_grid* gr, const double* qg, double rho0, double out[OR_NDIAG]);
 
 int or_num_threads(void);
+void or_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

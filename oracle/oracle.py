@@ -65,6 +65,7 @@ def lib():
         L.or_slope_solve.argtypes = [_dp, C.c_double, _dp, _dp]
         L.or_time_integrals.argtypes = [C.c_double, C.c_double, _dp]
         L.or_gp_flux.argtypes = [C.POINTER(Gas), _dp, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp]
+        L.or_set_num_threads.argtypes = [C.c_int]
         L.or_weno5z_right.restype = C.c_double
         L.or_weno5z_right.argtypes = [_dp]
         L.or_weno5z_left.restype = C.c_double
@@ -308,3 +309,8 @@ def plane_stats(gas: Gas, q: np.ndarray, dx=None, grid: Grid | None = None) -> n
 
 def num_threads() -> int:
     return lib().or_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """Host threads of the OpenMP loops (n <= 0: all cores)."""
+    lib().or_set_num_threads(int(n))

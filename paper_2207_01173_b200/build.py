@@ -34,13 +34,13 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     out = out or LIB
     if os.sep not in out:  # bare file name: a variant next to the default library
         out = os.path.join(os.path.dirname(LIB), out)
-    if not force and os.path.exists(out) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(s) for s in srcs):
         return out
     inc, nccl_so, nccl_dir = _nccl_dirs()
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            *["-D" + d for d in defines], *extra, "-I", INCLUDE, "-I", inc, "-o", out, os.path.join(CSRC, "hgks.cu"), "-L" + nccl_dir,
-           "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir] + (["-rdc=false"] if False else [])
+           "-Xlinker", "-l:" + os.path.basename(nccl_so), "-Xlinker", "-rpath," + nccl_dir]
     subprocess.check_call(cmd)
     return out
 

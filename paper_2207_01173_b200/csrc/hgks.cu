@@ -17,6 +17,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/hgks.h"
@@ -97,7 +98,9 @@ struct hgks_ctx {
   bool have_state = false;
   cudaStream_t s = nullptr;
   bool own_stream = false;
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;       // reductions (compute stream s)
+  ncclComm_t comm_halo = nullptr;  // z-halo send/recv (communication stream sc): a communicator of
+                                   // its own (ncclCommSplit), so the two streams never share one
   hgks_halo_plan plan{};
   int dev = 0;
   long long total_launches = 0;
@@ -125,6 +128,48 @@ static int fail(hgks_ctx* c, int code, const char* fmt, ...) {
   do {                                                                                      \
     ncclResult_t r_ = (call);                                                               \
     if (r_ != ncclSuccess) return fail((c), HGKS_ENCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+// Wait for the compute stream.  With NCCL, poll instead of blocking so that a failed or hung peer
+// surfaces as HGKS_ENCCL (ncclCommGetAsyncError, or no progress for HGKS_NCCL_TIMEOUT_S seconds,
+// default 300) and the communicators are aborted, rather than blocking the caller forever.
+static void abort_comms(hgks_ctx* c) {
+  if (c->comm_halo) ncclCommAbort(c->comm_halo);
+  if (c->comm) ncclCommAbort(c->comm);
+  c->comm_halo = c->comm = nullptr;
+}
+static int sync_s(hgks_ctx* c) {
+  if (!c->comm) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->s));
+    return HGKS_OK;
+  }
+  static const double timeout_s = [] {
+    const char* e = getenv("HGKS_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 300.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(c->s);
+    if (e == cudaSuccess) return HGKS_OK;
+    if (e != cudaErrorNotReady) return fail(c, HGKS_ECUDA, "stream: %s", cudaGetErrorString(e));
+    for (ncclComm_t cm : {c->comm, c->comm_halo}) {
+      ncclResult_t ar = ncclSuccess;
+      if (cm && ncclCommGetAsyncError(cm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        abort_comms(c);
+        return fail(c, HGKS_ENCCL, "NCCL asynchronous error: %s (communicators aborted)", ncclGetErrorString(ar));
+      }
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+      abort_comms(c);
+      return fail(c, HGKS_ENCCL, "no progress for %.0f s (a peer rank is gone?); communicators aborted", timeout_s);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+#define SYNC_TRY(c)              \
+  do {                           \
+    const int rc_ = sync_s(c);   \
+    if (rc_) return rc_;         \
   } while (0)
 
 // ---- instrumentation ------------------------------------------------------------------------
@@ -326,10 +371,10 @@ static int coll_halo(hgks_ctx* c, void* q, size_t esz) {
   } else if (c->comm) {  // one grouped send/recv per neighbour (Alg. 2; O-22: no ordering needed)
     ncclDataType_t ty = esz == 8 ? ncclFloat64 : ncclFloat32;
     NCCL_TRY(c, ncclGroupStart());
-    NCCL_TRY(c, ncclSend(b + pl.send_up * esz, pl.count, ty, pl.up, c->comm, c->sc));
-    NCCL_TRY(c, ncclRecv(b + pl.recv_down * esz, pl.count, ty, pl.down, c->comm, c->sc));
-    NCCL_TRY(c, ncclSend(b + pl.send_down * esz, pl.count, ty, pl.down, c->comm, c->sc));
-    NCCL_TRY(c, ncclRecv(b + pl.recv_up * esz, pl.count, ty, pl.up, c->comm, c->sc));
+    NCCL_TRY(c, ncclSend(b + pl.send_up * esz, pl.count, ty, pl.up, c->comm_halo, c->sc));
+    NCCL_TRY(c, ncclRecv(b + pl.recv_down * esz, pl.count, ty, pl.down, c->comm_halo, c->sc));
+    NCCL_TRY(c, ncclSend(b + pl.send_down * esz, pl.count, ty, pl.down, c->comm_halo, c->sc));
+    NCCL_TRY(c, ncclRecv(b + pl.recv_up * esz, pl.count, ty, pl.up, c->comm_halo, c->sc));
     NCCL_TRY(c, ncclGroupEnd());
   } else {  // loopback: pull both ghost chunks from the neighbours' buffers
     LoopGroup* G = c->grp;
@@ -607,7 +652,7 @@ static int diagnostics_t(hgks_ctx* c) {
   CUDA_TRY(c, cudaGetLastError());
   if ((rc = coll_allreduce(c, out, NDIAG, 1))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(c->diag_host, out, NDIAG * sizeof(double), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   return HGKS_OK;
 }
 
@@ -749,6 +794,10 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     if (p->stretch[d] == HGKS_TANH && !(p->stretch_b[d] > 0.0)) return fail(nullptr, HGKS_EINVAL, "stretch_b[%d] must be > 0", d);
     if (p->bc[d] == HGKS_WALL_ISOTHERMAL && !(p->T_wall > 0.0)) return fail(nullptr, HGKS_EINVAL, "T_wall must be > 0 with walls");
   }
+  // walls on both in-plane axes (a duct) would need the corner ghosts mirrored along both axes;
+  // the paper's wall-bounded case is the channel (walls in y only)
+  if (p->bc[0] == HGKS_WALL_ISOTHERMAL && p->bc[1] == HGKS_WALL_ISOTHERMAL)
+    return fail(nullptr, HGKS_EINVAL, "walls on both x and y are not supported (corner ghosts); use one wall axis");
   if (!(p->gamma > 1.0 && p->gamma <= 5.0 / 3.0 + 1e-12)) return fail(nullptr, HGKS_EINVAL, "gamma=%g outside (1, 5/3]", p->gamma);
   if (!(p->prandtl > 0.0)) return fail(nullptr, HGKS_EINVAL, "prandtl=%g must be > 0", p->prandtl);
   if (!(p->mu_ref >= 0.0)) return fail(nullptr, HGKS_EINVAL, "mu_ref < 0");
@@ -798,7 +847,9 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   if (p->stream) {
     c->s = (cudaStream_t)p->stream;
   } else {
-    if (cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) != cudaSuccess) {
+    // a BLOCKING stream: it orders with the legacy default stream, so a device buffer written by
+    // pending legacy-stream work (torch's default stream) is complete before set_state reads it
+    if (cudaStreamCreateWithFlags(&c->s, cudaStreamDefault) != cudaSuccess) {
       fail(c, HGKS_ECUDA, "stream creation failed");
       return bail(HGKS_ECUDA);
     }
@@ -913,6 +964,12 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
       c->comm = nullptr;
       return bail(HGKS_ENCCL);
     }
+    r = ncclCommSplit(c->comm, 0, p->rank, &c->comm_halo, nullptr);
+    if (r != ncclSuccess) {
+      fail(c, HGKS_ENCCL, "ncclCommSplit (halo communicator): %s", ncclGetErrorString(r));
+      c->comm_halo = nullptr;
+      return bail(HGKS_ENCCL);
+    }
   }
   *out = c;
   return HGKS_OK;
@@ -937,7 +994,7 @@ static int set_state_t(hgks_ctx* c) {
   if (c->p.force_mode != HGKS_FORCE_NONE && (rc = diagnostics_t<T>(c))) return rc;  // bulk of Q^0 (O-27)
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   if (c->p.force_mode != HGKS_FORCE_NONE) {  // restart the controller from this state
     const double* a = c->diag_host;
     h->volume = a[HGKS_DIAG_VOLUME];
@@ -957,7 +1014,7 @@ static int set_state_t(hgks_ctx* c) {
   CUDA_TRY(c, cudaGetLastError());
   if ((rc = coll_allreduce(c, &c->ctl->red[0], 2, 0))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   if (h->red[1]) {
     if (h->bad_cell != ~0ull) {
       unsigned long long b = h->bad_cell;
@@ -969,7 +1026,7 @@ static int set_state_t(hgks_ctx* c) {
   h->smax_cur = h->red[0];
   h->red[0] = 0;
   CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   c->have_state = true;
   return HGKS_OK;
 }
@@ -996,7 +1053,7 @@ int hgks_get_state(hgks_ctx* c, double* q, int on_device) {
   c->total_launches += 1;
   CUDA_TRY(c, cudaGetLastError());
   CUDA_TRY(c, cudaMemcpyAsync(q, c->stage64, 5 * ncell * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   return HGKS_OK;
 }
 
@@ -1009,7 +1066,7 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   // reset per-call control: t, t_end, counters (one small H2D copy)
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   h->t = *t_inout;
   h->t_end = t_end;
   h->halt = 0;
@@ -1027,7 +1084,7 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
     int rc = c->fp32 ? run_steps_graphed<float>(c, n) : run_steps_graphed<double>(c, n);
     if (rc) return rc;
     CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-    CUDA_TRY(c, cudaStreamSynchronize(c->s));
+    SYNC_TRY(c);
     if (h->halt || n <= 0) break;
   }
   c->cur = cur0 ^ (int)(h->steps_done & 1);  // buffer holding the last committed state
@@ -1081,7 +1138,7 @@ static int plane_stats_t(hgks_ctx* c, double* out) {
   int rc;
   if ((rc = coll_allreduce(c, c->stats_dev, cnt, 1))) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(out, c->stats_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   const double inv = 1.0 / ((double)c->n[0] * c->n[2]);
   for (size_t k = 0; k < cnt; ++k) out[k] *= inv;
   return HGKS_OK;
@@ -1103,7 +1160,7 @@ int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* 
   CUDA_TRY(c, cudaSetDevice(c->dev));
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   const bool b = c->p.force_mode == HGKS_FORCE_BULK;
   if (force) *force = h->f_prev;
   if (bulk_momentum) *bulk_momentum = b ? h->m_cur : 0.0;
@@ -1122,6 +1179,7 @@ int hgks_destroy(hgks_ctx* c) {
   if (c->sc) cudaStreamSynchronize(c->sc);
   for (int b = 0; b < 2; ++b)
     if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
+  if (c->comm_halo) ncclCommDestroy(c->comm_halo);
   if (c->comm) ncclCommDestroy(c->comm);
   lb_leave(c);
   cudaFree(c->red_tmp);
@@ -1156,7 +1214,7 @@ int hgks_destroy(hgks_ctx* c) {
 
 int hgks_profile_enable(hgks_ctx* c, int enable) {
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_profile_enable: ctx is NULL");
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   if (enable && !c->prof.created) {
     for (int k = 0; k < 2 * 4096; ++k) CUDA_TRY(c, cudaEventCreate(&c->prof.ev[k]));
     c->prof.created = true;
@@ -1173,7 +1231,7 @@ int hgks_profile_enable(hgks_ctx* c, int enable) {
 
 int hgks_profile_read(hgks_ctx* c, double ms[HGKS_K_COUNT], int64_t launches[HGKS_K_COUNT], int64_t* total_launches) {
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_profile_read: ctx is NULL");
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   prof_flush(c);
   for (int k = 0; k < HGKS_K_COUNT; ++k) {
     if (ms) ms[k] = c->prof.ms[k];
@@ -1224,7 +1282,7 @@ static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
   T* Q = (T*)c->Q[c->cur];
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   h->dt = dt;
   h->halt = 0;
   CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
@@ -1251,7 +1309,7 @@ extern "C" {
 int hgks_test_face_flux(hgks_ctx* c, int dir, double* out) {
   if (!c || !out || dir < 0 || dir > 2) return fail(c, HGKS_EINVAL, "hgks_test_face_flux: bad arguments");
   const size_t n = 10 * c->nface[dir];
-  CUDA_TRY(c, cudaStreamSynchronize(c->s));
+  SYNC_TRY(c);
   if (c->fp32) {
     float* h = (float*)malloc(n * sizeof(float));
     cudaError_t e = cudaMemcpy(h, c->F[dir], n * sizeof(float), cudaMemcpyDeviceToHost);

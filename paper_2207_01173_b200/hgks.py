@@ -180,6 +180,9 @@ def _ptr(q):
     import torch  # noqa: PLC0415 (torch only for device memory)
     if not isinstance(q, torch.Tensor) or q.dtype != torch.float64 or not q.is_contiguous():
         raise TypeError("state must be a contiguous float64 torch tensor or numpy array")
+    if q.is_cuda:
+        # the library's stream does not know the tensor's producer: finish pending torch work first
+        torch.cuda.current_stream(q.device).synchronize()
     return q.data_ptr(), int(q.is_cuda)
 
 

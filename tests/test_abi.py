@@ -64,7 +64,8 @@ def test_create_validates_before_device():
            dict(bc=(0, 1, 0), T_wall=0.0),
            dict(nranks=2, rank=0), dict(n=(8, 8, 5), nranks=2, rank=1, nccl_id=b"x" * 128),
            dict(nranks=2, rank=0, nccl_id=b"x" * 128, group_key=7),  # NCCL and loopback are exclusive
-           dict(n=(8, 8, 60), nranks=17, rank=0, group_key=7)]       # loopback group: <= 16 ranks
+           dict(n=(8, 8, 60), nranks=17, rank=0, group_key=7),       # loopback group: <= 16 ranks
+           dict(bc=(1, 1, 0), T_wall=1.0)]                            # walls on x AND y (duct corners)
     for kw in bad:
         args = dict(n=(8, 8, 8), lo=(0, 0, 0), hi=(1, 1, 1))
         args.update(kw)

@@ -1,0 +1,53 @@
+// Microbenchmark: the ALU peaks bench.py divides by (roofline.peak for the FP64 and FP32 flux).
+// Dependent-chain-free FMA loops (8 independent chains per thread, 4 blocks x 256 threads per SM)
+// for DFMA (fp64) and FFMA (fp32); prints one JSON object.  Build + run on a B200:
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/alu_peaks tools/microbench/alu_peaks.cu && /tmp/alu_peaks
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <typename T>
+__global__ void fma_loop(T* out, int iters, T seed) {
+  T x[8];
+  for (int k = 0; k < 8; ++k) x[k] = seed + T(k) + T(threadIdx.x);
+  const T a = T(0.999999), b = T(1e-7);
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  T acc = T(0);
+  for (int k = 0; k < 8; ++k) acc += x[k];
+  if (acc == T(12345.678)) out[0] = acc;
+}
+
+template <typename T>
+static double tflops(int blocks, int threads, int iters) {
+  T* out;
+  cudaMalloc(&out, sizeof(T));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    fma_loop<T><<<blocks, threads>>>(out, iters, T(1));
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = (double)blocks * threads * iters * 8 * 2;
+    if (rep > 0 && fl / ms / 1e9 > best) best = fl / ms / 1e9;
+  }
+  cudaFree(out);
+  return best;
+}
+
+int main() {
+  int sms, clk_khz;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  const double d = tflops<double>(sms * 4, 256, 20000);
+  const double f = tflops<float>(sms * 4, 256, 40000);
+  printf("{\"dfma_tflops\": %.3f, \"ffma_tflops\": %.3f, \"sms\": %d, \"clock_rate_mhz_attr\": %.0f, "
+         "\"how\": \"tools/microbench/alu_peaks.cu: 8 independent FMA chains per thread, %d blocks x 256, best of 4\"}\n",
+         d, f, sms, clk_khz / 1000.0, sms * 4);
+  return 0;
+}
