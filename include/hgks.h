@@ -161,6 +161,23 @@ typedef enum {
 } hgks_diag;
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]);
 
+/* Per-step diagnostic history (time histories of E_k, eps_com, enstrophy, Figs 7-8):
+ * with capacity > 0 every following hgks_step computes the volume diagnostics of hgks_diagnostics
+ * for the state at the START of each step, fused into that step's stage-1 update kernel (Q^n with the
+ * ghosts its halo has just filled; fixed-order per-block sums, two fixed-order reduction kernels,
+ * fp64 for either precision; no host round trip).  capacity = rows held on the device (each row is
+ * read once); rho0 > 0 normalises as hgks_diagnostics.  capacity 0 disables (the default).  Frees
+ * and re-allocates the history buffers; the rows pending are discarded.
+ * Errors: HGKS_EINVAL (capacity < 0, rho0 <= 0), HGKS_ENOMEM, HGKS_ECUDA. */
+#define HGKS_HIST_COLS (2 + HGKS_DIAG_COUNT) /* t, dt, then the hgks_diag order */
+int hgks_history_enable(hgks_ctx* c, int32_t capacity, double rho0);
+
+/* Read and clear the rows recorded since the last read: out[r * HGKS_HIST_COLS + k], k = 0: t of the
+ * step's start state, 1: the step's dt, 2..: hgks_diagnostics of that state.  *rows = rows written
+ * (<= max_rows, else HGKS_EINVAL and nothing is consumed).  Collective: one NCCL sum of all rows.
+ * hgks_step refuses (HGKS_EINVAL) a call that could overflow the capacity.  Synchronises. */
+int hgks_history_read(hgks_ctx* c, double* out, int32_t max_rows, int32_t* rows);
+
 /* x-z plane means of the current state for every GLOBAL y index j (channel statistics, P:1186-1238;
  * the paper's <.> averages over time and the X and Z directions, P:1190-1191 -- time averaging is
  * left to the caller, who samples this every few steps).  out[j * HGKS_STAT_COUNT + s], j < ny,

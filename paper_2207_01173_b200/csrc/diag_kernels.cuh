@@ -12,13 +12,7 @@
 
 namespace hgks {
 
-constexpr int NDIAG = 11;  // HGKS_DIAG_COUNT
 constexpr int DIAG_BLOCKS = 148 * 4;
-
-template <typename T>
-__device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& g, int c, int i, int j, int k) {
-  return (double)q[qidx(g, 1 + c, i, j, k)] / (double)q[qidx(g, 0, i, j, k)];
-}
 
 template <typename T>
 __global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q, Geo<T> g, DiagGeo dg, double gamma,
@@ -31,44 +25,7 @@ __global__ void __launch_bounds__(DIAG_TPB) diag_kernel(const T* __restrict__ q,
   const long long ncell = (long long)nx * ny * g.n[2];
   for (long long e = blockIdx.x * (long long)DIAG_TPB + threadIdx.x; e < ncell; e += (long long)gridDim.x * DIAG_TPB) {
     const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
-    const int ijk[3] = {i, j, k};
-    const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
-    const double rho = (double)q[qidx(g, 0, i, j, k)];
-    double u[3], m[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      m[c] = (double)q[qidx(g, 1 + c, i, j, k)];
-      u[c] = m[c] / rho;
-    }
-    double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double J = dg.jc[d][ijk[d]];
-      const int di = d == 0, dj = d == 1, dk = d == 2;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double d1 = vel_of(q, g, c, i + di, j + dj, k + dk) - vel_of(q, g, c, i - di, j - dj, k - dk);
-        const double d2 = vel_of(q, g, c, i + 2 * di, j + 2 * dj, k + 2 * dk) -
-                          vel_of(q, g, c, i - 2 * di, j - 2 * dj, k - 2 * dk);
-        grad[c][d] = J * (8.0 * d1 - d2) / 12.0;
-      }
-    }
-    const double o0 = grad[2][1] - grad[1][2], o1 = grad[0][2] - grad[2][0], o2 = grad[1][0] - grad[0][1];
-    const double om2 = o0 * o0 + o1 * o1 + o2 * o2;
-    const double dv = grad[0][0] + grad[1][1] + grad[2][2];
-    acc[0] += 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * vol;
-    acc[1] += 0.5 * rho * om2 * vol;
-    acc[2] += om2 * vol;
-    acc[3] += dv * dv * vol;
-    acc[4] += rho * vol;
-    acc[5] += m[0] * vol;
-    acc[6] += m[1] * vol;
-    acc[7] += m[2] * vol;
-    const double rhoE = (double)q[qidx(g, 4, i, j, k)];
-    acc[8] += rhoE * vol;
-    acc[9] += vol;
-    const double p = (gamma - 1.0) * (rhoE - 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]));
-    acc[10] += p * dv * vol;  // pressure-dilatation
+    diag_cell(q, g, dg, gamma, i, j, k, acc);
   }
   block_sum_fixed(acc, sh);
   if (threadIdx.x == 0) {

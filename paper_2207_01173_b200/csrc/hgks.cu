@@ -76,6 +76,13 @@ struct hgks_ctx {
   double* diag_host = nullptr;  // pinned NDIAG
   double* stats_dev = nullptr;  // ny * NSTAT plane sums (hgks_plane_stats)
   double* bulk_dev = nullptr;   // 2 per update block: (sum rho dV, sum rho U dV) partials (O-27)
+  // per-step diagnostic history (hgks_history_enable): NDIAG partials per update block, HIST_RB second
+  // level partials, rows [cap][NDIAG] of rank-local sums and [cap][2] (t, dt)
+  double *dpart = nullptr, *dpart2 = nullptr, *hist = nullptr, *hist_td = nullptr;
+  int hist_cap = 0;
+  long long hist_pending = 0;  // upper bound of rows written since the last read (host)
+  double hist_rho0 = 1.0;
+  size_t red_tmp_count = 0;
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
   cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
@@ -348,6 +355,7 @@ static int coll_allreduce(hgks_ctx* c, void* buf, size_t count, int op) {
     src.p[q] = G->ptr[q];
     if (q != r) CUDA_TRY(c, cudaStreamWaitEvent(c->s, G->m[q]->lb_rpost, 0));
   }
+  if (count > c->red_tmp_count) return fail(c, HGKS_EINVAL, "loopback allreduce of %zu > %zu elements", count, c->red_tmp_count);
   lb_reduce_kernel<<<(int)std::min<size_t>((count + 255) / 256, 64), 256, 0, c->s>>>(src, n, (long long)count, op, c->red_tmp);
   c->total_launches += 1;
   CUDA_TRY(c, cudaGetLastError());
@@ -678,8 +686,16 @@ static int run_steps(hgks_ctx* c, int nsteps) {
     if ((rc = fill_ghosts<T>(c, Qn, false))) return rc;
     if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
-    update_kernel<T, 1><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
-                                                   c->ctl, c->bulk_dev);
+    if (c->hist_cap > 0) {  // + volume diagnostics of Q^n (per-step history, NEXT-2)
+      update_kernel<T, 1, true><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg,
+                                                           c->p.gamma, c->ctl, c->bulk_dev, c->dpart);
+      hist_reduce_kernel<<<HIST_RB, DIAG_TPB, 0, c->s>>>(c->dpart, ublocks, c->dpart2, c->ctl);
+      hist_final_kernel<<<1, DIAG_TPB, 0, c->s>>>(c->dpart2, c->hist, c->hist_td, c->ctl);
+      c->total_launches += 2;
+    } else {
+      update_kernel<T, 1><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg, c->p.gamma,
+                                                     c->ctl, c->bulk_dev);
+    }
     prof_end(c, HGKS_K_UPDATE);
     // stage 2 at Q* (same dt and windows, O-11)
     if ((rc = fill_ghosts<T>(c, Qs, false))) return rc;
@@ -886,7 +902,8 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   ok = ok && cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess;
   for (cudaEvent_t* e : {&c->ev_xy, &c->ev_halo, &c->lb_post, &c->lb_done, &c->lb_rpost, &c->lb_rdone})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
-  ok = ok && cudaMalloc(&c->red_tmp, ((size_t)c->n[1] * NSTAT + NDIAG + 16) * 8) == cudaSuccess;  // largest allreduce
+  c->red_tmp_count = (size_t)c->n[1] * NSTAT + NDIAG + 16;  // largest allreduce (history rows: resized)
+  ok = ok && cudaMalloc(&c->red_tmp, c->red_tmp_count * 8) == cudaSuccess;
   for (int d = 0; d < 3; ++d) {
     ok = ok && cudaEventCreateWithFlags(&c->ev_rec[d], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_flux[d], cudaEventDisableTiming) == cudaSuccess;
@@ -1062,7 +1079,11 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   if (!t_inout) return fail(c, HGKS_EINVAL, "hgks_step: t_inout is NULL");
   if (nsteps < 0) return fail(c, HGKS_EINVAL, "hgks_step: nsteps < 0");
   if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_step: call hgks_set_state first");
+  if (c->hist_cap > 0 && c->hist_pending + nsteps > c->hist_cap)
+    return fail(c, HGKS_EINVAL, "hgks_step: %d steps would overflow the diagnostic history (%lld of %d rows pending; "
+                "call hgks_history_read)", nsteps, c->hist_pending, c->hist_cap);
   CUDA_TRY(c, cudaSetDevice(c->dev));
+  if (c->hist_cap > 0) c->hist_pending += nsteps;
   // reset per-call control: t, t_end, counters (one small H2D copy)
   Ctl* h = c->ctl_host;
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
@@ -1106,6 +1127,98 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
 
 extern "C" {
 
+}  // extern "C"
+
+// raw volume sums a[NDIAG] -> the hgks_diagnostics normalisation (O-24, O-25)
+static void normalise_diag(const hgks_ctx* c, double rho0, const double* a, double* out) {
+  const double vol = a[HGKS_DIAG_VOLUME], mu = c->p.mu_ref;
+  for (int k = 0; k < NDIAG; ++k) out[k] = a[k];
+  out[HGKS_DIAG_EK] = a[HGKS_DIAG_EK] / (rho0 * vol);
+  out[HGKS_DIAG_ENSTROPHY] = a[HGKS_DIAG_ENSTROPHY] / (rho0 * vol);
+  out[HGKS_DIAG_EPS_S] = mu * a[HGKS_DIAG_EPS_S] / (rho0 * vol);
+  out[HGKS_DIAG_EPS_D] = 4.0 / 3.0 * mu * a[HGKS_DIAG_EPS_D] / (rho0 * vol);
+  out[HGKS_DIAG_PDIL] = a[HGKS_DIAG_PDIL] / (rho0 * vol);
+}
+
+static int set_ctl_hist(hgks_ctx* c, int n, int cap) {
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  SYNC_TRY(c);
+  h->hist_n = n;
+  h->hist_cap = cap;
+  CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
+  SYNC_TRY(c);
+  return HGKS_OK;
+}
+
+extern "C" {
+
+int hgks_history_enable(hgks_ctx* c, int32_t capacity, double rho0) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_history_enable: ctx is NULL");
+  if (capacity < 0 || !(rho0 > 0.0)) return fail(c, HGKS_EINVAL, "hgks_history_enable: capacity < 0 or rho0 <= 0");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  SYNC_TRY(c);
+  for (double** b : {&c->dpart, &c->dpart2, &c->hist, &c->hist_td}) {
+    cudaFree(*b);
+    *b = nullptr;
+  }
+  for (int b = 0; b < 2; ++b)  // captured graphs hold the update variant: recapture
+    if (c->gexec[b]) {
+      cudaGraphExecDestroy(c->gexec[b]);
+      c->gexec[b] = nullptr;
+    }
+  c->hist_cap = 0;
+  c->hist_pending = 0;
+  c->hist_rho0 = rho0;
+  if (capacity > 0) {
+    const size_t ublocks = (size_t)((c->n[0] + UPD_X - 1) / UPD_X) * ((c->n[1] + UPD_Y - 1) / UPD_Y) * c->nzl;
+    bool ok = cudaMalloc(&c->dpart, ublocks * NDIAG * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->dpart2, (size_t)HIST_RB * NDIAG * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->hist, (size_t)capacity * NDIAG * sizeof(double)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->hist_td, (size_t)capacity * 2 * sizeof(double)) == cudaSuccess;
+    if (ok && (size_t)capacity * NDIAG > c->red_tmp_count) {
+      cudaFree(c->red_tmp);
+      c->red_tmp_count = (size_t)capacity * NDIAG;
+      ok = cudaMalloc(&c->red_tmp, c->red_tmp_count * 8) == cudaSuccess;
+    }
+    if (!ok) {
+      cudaGetLastError();
+      return fail(c, HGKS_ENOMEM, "hgks_history_enable: device allocation failed");
+    }
+    c->hist_cap = capacity;
+  }
+  return set_ctl_hist(c, 0, c->hist_cap);
+}
+
+int hgks_history_read(hgks_ctx* c, double* out, int32_t max_rows, int32_t* rows) {
+  if (!c || !rows) return fail(c, HGKS_EINVAL, "hgks_history_read: NULL argument");
+  if (c->hist_cap <= 0) return fail(c, HGKS_EINVAL, "hgks_history_read: history not enabled");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  Ctl* h = c->ctl_host;
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  SYNC_TRY(c);
+  const int n = h->hist_n;
+  if (n > max_rows || (n > 0 && !out))
+    return fail(c, HGKS_EINVAL, "hgks_history_read: %d rows pending, buffer holds %d", n, max_rows);
+  *rows = n;
+  if (n > 0) {
+    int rc;
+    if ((rc = coll_allreduce(c, c->hist, (size_t)n * NDIAG, 1))) return rc;  // rank-local sums -> global
+    std::vector<double> a((size_t)n * NDIAG), td((size_t)n * 2);
+    CUDA_TRY(c, cudaMemcpyAsync(a.data(), c->hist, a.size() * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(c, cudaMemcpyAsync(td.data(), c->hist_td, td.size() * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    SYNC_TRY(c);
+    for (int r = 0; r < n; ++r) {
+      double* o = out + (size_t)r * HGKS_HIST_COLS;
+      o[0] = td[2 * r];
+      o[1] = td[2 * r + 1];
+      normalise_diag(c, c->hist_rho0, &a[(size_t)r * NDIAG], o + 2);
+    }
+  }
+  c->hist_pending = 0;
+  return set_ctl_hist(c, 0, c->hist_cap);
+}
+
 int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_diagnostics: ctx is NULL");
   if (!out) return fail(c, HGKS_EINVAL, "hgks_diagnostics: out is NULL");
@@ -1115,14 +1228,7 @@ int hgks_diagnostics(hgks_ctx* c, double rho0, double out[HGKS_DIAG_COUNT]) {
   CUDA_TRY(c, cudaSetDevice(c->dev));
   int rc = c->fp32 ? diagnostics_t<float>(c) : diagnostics_t<double>(c);
   if (rc) return rc;
-  const double* a = c->diag_host;
-  const double vol = a[HGKS_DIAG_VOLUME], mu = c->p.mu_ref;
-  for (int k = 0; k < NDIAG; ++k) out[k] = a[k];
-  out[HGKS_DIAG_EK] = a[HGKS_DIAG_EK] / (rho0 * vol);
-  out[HGKS_DIAG_ENSTROPHY] = a[HGKS_DIAG_ENSTROPHY] / (rho0 * vol);
-  out[HGKS_DIAG_EPS_S] = mu * a[HGKS_DIAG_EPS_S] / (rho0 * vol);
-  out[HGKS_DIAG_EPS_D] = 4.0 / 3.0 * mu * a[HGKS_DIAG_EPS_D] / (rho0 * vol);
-  out[HGKS_DIAG_PDIL] = a[HGKS_DIAG_PDIL] / (rho0 * vol);
+  normalise_diag(c, rho0, c->diag_host, out);
   return HGKS_OK;
 }
 
@@ -1195,6 +1301,7 @@ int hgks_destroy(hgks_ctx* c) {
   cudaFree(c->diag_dev);
   cudaFree(c->bulk_dev);
   cudaFree(c->stats_dev);
+  for (double* b : {c->dpart, c->dpart2, c->hist, c->hist_td}) cudaFree(b);
   if (c->diag_host) cudaFreeHost(c->diag_host);
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->ev_in) cudaEventDestroy(c->ev_in);

@@ -43,6 +43,7 @@ struct Ctl {
   double m_cur, rho_cur;        // bulk momentum / density of the committed state
   double m_prev, dt_prev, f_prev;  // controller memory: previous step's m, dt and f
   double bulk_new[2];           // (sum rho dV, sum rho U dV) of the newest state (allreduced)
+  int hist_n, hist_cap;         // per-step diagnostic history: rows written / capacity
 };
 
 template <typename T>
@@ -94,6 +95,86 @@ __device__ __forceinline__ void block_sum_fixed(double (&v)[N], double* sh) {
 template <typename T>
 __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, int k) {
   return (long long)(k + 3) * g.plane + (long long)v * g.vs + (long long)(j + 3) * g.px + (i + 3);
+}
+
+// ---- volume diagnostics of one cell (readings O-24, O-25, O-29) --
+// acc += (1/2 rho|U|^2, 1/2 rho|omega|^2, |omega|^2, (div U)^2, rho, rho U, rho V, rho W, rho E, 1,
+//         p div U) dV, velocity derivatives by 4th-order central differences of the cell-average
+// velocities in the cell index times J = d(index)/dx at the cell centre (ghosts as filled).  fp64 for
+// either precision.  Used by diag_kernel (on demand) and by the stage-1 update (per-step history).
+constexpr int NDIAG = 11;  // HGKS_DIAG_COUNT
+
+template <typename T>
+__device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& g, int c, int i, int j, int k) {
+  return (double)q[qidx(g, 1 + c, i, j, k)] / (double)q[qidx(g, 0, i, j, k)];
+}
+
+template <typename T>
+__device__ __forceinline__ void diag_cell(const T* __restrict__ q, const Geo<T>& g, const DiagGeo& dg, double gamma, int i,
+                                          int j, int k, double (&acc)[NDIAG]) {
+  const int ijk[3] = {i, j, k};
+  const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
+  const double rho = (double)q[qidx(g, 0, i, j, k)];
+  double u[3], m[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    m[c] = (double)q[qidx(g, 1 + c, i, j, k)];
+    u[c] = m[c] / rho;
+  }
+  double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25)
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double J = dg.jc[d][ijk[d]];
+    const int di = d == 0, dj = d == 1, dk = d == 2;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double d1 = vel_of(q, g, c, i + di, j + dj, k + dk) - vel_of(q, g, c, i - di, j - dj, k - dk);
+      const double d2 = vel_of(q, g, c, i + 2 * di, j + 2 * dj, k + 2 * dk) - vel_of(q, g, c, i - 2 * di, j - 2 * dj, k - 2 * dk);
+      grad[c][d] = J * (8.0 * d1 - d2) / 12.0;
+    }
+  }
+  const double o0 = grad[2][1] - grad[1][2], o1 = grad[0][2] - grad[2][0], o2 = grad[1][0] - grad[0][1];
+  const double om2 = o0 * o0 + o1 * o1 + o2 * o2;
+  const double dv = grad[0][0] + grad[1][1] + grad[2][2];
+  const double u2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  acc[0] += 0.5 * rho * u2 * vol;
+  acc[1] += 0.5 * rho * om2 * vol;
+  acc[2] += om2 * vol;
+  acc[3] += dv * dv * vol;
+  acc[4] += rho * vol;
+  acc[5] += m[0] * vol;
+  acc[6] += m[1] * vol;
+  acc[7] += m[2] * vol;
+  const double rhoE = (double)q[qidx(g, 4, i, j, k)];
+  acc[8] += rhoE * vol;
+  acc[9] += vol;
+  const double p = (gamma - 1.0) * (rhoE - 0.5 * rho * u2);
+  acc[10] += p * dv * vol;  // pressure-dilatation (O-29)
+}
+
+// sum v[0..N) over a DIAG_TPB block in a fixed order (warp butterflies, then the warps in order);
+// result valid in thread 0.  sh: >= N * (DIAG_TPB / 32) doubles.
+template <int N>
+__device__ __forceinline__ void block_sum_warps(double (&v)[N], double* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[n] += __shfl_xor_sync(0xffffffffu, v[n], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) sh[n * (DIAG_TPB / 32) + w] = v[n];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      double s = 0.0;
+      for (int k = 0; k < DIAG_TPB / 32; ++k) s += sh[n * (DIAG_TPB / 32) + k];
+      v[n] = s;
+    }
+  }
 }
 
 #ifndef HGKS_FLUX_TPB
@@ -649,11 +730,17 @@ __device__ __forceinline__ void block_max_commit(double s, unsigned long long* d
 // Lt = L + dt/2 dL of Q^n, recovered from the two stage-1 outputs: with a = Q* - Q^n and
 // b = R - Q^n (a = dt L/2 + dt^2 dL/8, b = dt L + dt^2 dL/6), Lt = (8a - 3b)/dt.  Mode 2 also
 // sums (rho dV, rho U dV) of Q^{n+1} per block (fixed order) into bulk[2 * blockIdx.x + {0, 1}].
+// DIAG (stage 1 only; the per-step history of hgks_history_enable, NEXT-2): the volume diagnostics
+// of Q^n -- whose ghosts the stage-1 halo has just filled -- summed per block (fixed order) into
+// dpart[NDIAG * block]; hist_reduce_kernel / hist_final_kernel finish the sum.  Stage 2 cannot see
+// the gradients of Q^{n+1} (its neighbours are written by other blocks of the same launch), so the
+// history holds the state at the START of every step; the final state is one hgks_diagnostics call.
 constexpr int UPD_X = 64, UPD_Y = DIAG_TPB / UPD_X;  // update_kernel block shape (DIAG_TPB threads)
-template <typename T, int STAGE>
+template <typename T, int STAGE, bool DIAG = false>
 __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
-                              Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk) {
+                              Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk,
+                              double* __restrict__ dpart = nullptr) {
   if (ctl->halt) return;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   // block = UPD_X x UPD_Y cells of one z plane (grid: x tiles, y tiles, z): no index divisions
@@ -731,6 +818,19 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
       }
     }
   }
+  if (STAGE == 1 && DIAG) {
+    double acc[NDIAG];
+#pragma unroll
+    for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
+    if (i < nx && j < ny) diag_cell(Q, g, dg, gamma, i, j, k, acc);
+    __shared__ double shd[NDIAG * (DIAG_TPB / 32)];
+    block_sum_warps(acc, shd);
+    if (threadIdx.x == 0) {
+      const long long bid = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+      for (int n = 0; n < NDIAG; ++n) dpart[bid * NDIAG + n] = acc[n];
+    }
+  }
   if (STAGE == 2) {
     block_max_commit(smax, &ctl->red[0]);
     if (fmode == 2) {  // uniform branch: every thread of the block takes it
@@ -741,6 +841,55 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
         bulk[2 * bid] = bsum[0];
         bulk[2 * bid + 1] = bsum[1];
       }
+    }
+  }
+}
+
+// ---- per-step diagnostic history (NEXT-2) -------------------------------------------------------
+// hist_reduce_kernel: HIST_RB blocks, block b sums the update-block partials [b*per, (b+1)*per) in a
+// fixed order into dpart2[b]; hist_final_kernel (one block) sums dpart2 in order into row
+// ctl->hist_n of hist[cap][NDIAG] and records (t, dt) of the step in hist_td[cap][2].
+constexpr int HIST_RB = 148;
+__global__ void __launch_bounds__(DIAG_TPB) hist_reduce_kernel(const double* __restrict__ dpart, long long nblocks,
+                                                               double* __restrict__ dpart2, const Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  __shared__ double sh[NDIAG * (DIAG_TPB / 32)];
+  const long long per = (nblocks + gridDim.x - 1) / gridDim.x;
+  const long long b0 = blockIdx.x * per, b1 = min(nblocks, b0 + per);
+  double acc[NDIAG];
+#pragma unroll
+  for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
+  for (long long b = b0 + threadIdx.x; b < b1; b += DIAG_TPB) {
+#pragma unroll
+    for (int n = 0; n < NDIAG; ++n) acc[n] += dpart[b * NDIAG + n];
+  }
+  block_sum_warps(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < NDIAG; ++n) dpart2[blockIdx.x * NDIAG + n] = acc[n];
+  }
+}
+
+__global__ void __launch_bounds__(DIAG_TPB) hist_final_kernel(const double* __restrict__ dpart2, double* __restrict__ hist,
+                                                              double* __restrict__ hist_td, Ctl* __restrict__ ctl) {
+  if (ctl->halt) return;
+  __shared__ double sh[NDIAG * (DIAG_TPB / 32)];
+  double acc[NDIAG];
+#pragma unroll
+  for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
+  for (int b = threadIdx.x; b < HIST_RB; b += DIAG_TPB) {
+#pragma unroll
+    for (int n = 0; n < NDIAG; ++n) acc[n] += dpart2[b * NDIAG + n];
+  }
+  block_sum_warps(acc, sh);
+  if (threadIdx.x == 0) {
+    const int row = ctl->hist_n;
+    if (row < ctl->hist_cap) {
+#pragma unroll
+      for (int n = 0; n < NDIAG; ++n) hist[(long long)row * NDIAG + n] = acc[n];
+      hist_td[2 * row] = ctl->t;
+      hist_td[2 * row + 1] = ctl->dt;
+      ctl->hist_n = row + 1;
     }
   }
 }

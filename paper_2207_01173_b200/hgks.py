@@ -34,7 +34,7 @@ KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt",
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_diagnostics", "hgks_plane_stats", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+            "hgks_diagnostics", "hgks_history_enable", "hgks_history_read", "hgks_plane_stats", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
 STAT_NAMES = ("rho", "U", "V", "W", "UU", "VV", "WW", "UV", "rhoU", "rhoV", "rhoUV", "c", "M", "MM", "T", "p")
 DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume",
               "p_dil")
@@ -90,6 +90,8 @@ def lib():
         L.hgks_make_halo_plan.argtypes = [C.c_int32] * 5 + [C.POINTER(HaloPlan)]
         L.hgks_diagnostics.argtypes = [vp, C.c_double, _dp]
         L.hgks_get_forcing.argtypes = [vp, _dp, _dp, _dp]
+        L.hgks_history_enable.argtypes = [vp, C.c_int32, C.c_double]
+        L.hgks_history_read.argtypes = [vp, _dp, C.c_int32, C.POINTER(C.c_int32)]
         L.hgks_plane_stats.argtypes = [vp, _dp]
         L.hgks_profile_enable.argtypes = [vp, C.c_int]
         L.hgks_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -208,6 +210,23 @@ def hgks_diagnostics(ctx, rho0: float = 1.0) -> np.ndarray:
     out = np.zeros(len(DIAG_NAMES))
     _check(lib().hgks_diagnostics(ctx, rho0, out.ctypes.data_as(_dp)), ctx)
     return out
+
+
+HIST_COLS = 2 + len(DIAG_NAMES)  # t, dt, DIAG_NAMES
+
+
+def hgks_history_enable(ctx, capacity: int, rho0: float = 1.0) -> None:
+    """Record the volume diagnostics of the start state of every following step (fused into the
+    stage-1 update; capacity rows on the device; 0 disables)."""
+    _check(lib().hgks_history_enable(ctx, int(capacity), float(rho0)), ctx)
+
+
+def hgks_history_read(ctx, max_rows: int) -> np.ndarray:
+    """[rows][HIST_COLS] = (t, dt, DIAG_NAMES...) of the steps since the last read (collective)."""
+    out = np.zeros((max(max_rows, 1), HIST_COLS))
+    n = C.c_int32()
+    _check(lib().hgks_history_read(ctx, out.ctypes.data_as(_dp), int(max_rows), C.byref(n)), ctx)
+    return out[:n.value]
 
 
 def hgks_plane_stats(ctx, ny: int) -> np.ndarray:

@@ -99,3 +99,37 @@ def test_tgv_conservation_and_decay_on_gpu():
     for k in ("mom_x", "mom_y", "mom_z"):
         assert abs(d1[i[k]] - d0[i[k]]) <= 1e-13 * mom_scale
     assert d1[i["E_k"]] < d0[i["E_k"]]
+
+
+@pytest.mark.parametrize("precision", [H.HGKS_FP64, H.HGKS_FP32])
+def test_per_step_history_matches_oracle(precision):
+    """NEXT-2 time histories: the diagnostics fused into the stage-1 update hold, for
+    every step, the state at the START of the step.  Each row must match or_diagnostics of the state
+    the GPU had there (read back step by step in a twin context), and (t, dt) the step's."""
+    n = 32
+    q, dx = inputs.tgv(n)
+    prm = inputs.tgv_params()
+    gas = O.make_gas(mu=prm["mu"])
+    kw = dict(mu=prm["mu"], precision=precision, cfl=0.4)
+    with H.Solver((n, n, n), (-math.pi,) * 3, (math.pi,) * 3, **kw) as s, \
+            H.Solver((n, n, n), (-math.pi,) * 3, (math.pi,) * 3, **kw) as twin:
+        H.hgks_history_enable(s.ctx, 16, rho0=1.0)
+        s.set_state(q)
+        twin.set_state(q)
+        s.step(6)
+        s.step(4)
+        rows = H.hgks_history_read(s.ctx, 16)
+        assert rows.shape == (10, H.HIST_COLS)
+        t = 0.0
+        for r in range(10):
+            qs = twin.get_state()
+            ref = O.diagnostics(gas, qs, (2 * math.pi / n,) * 3)
+            _compare(rows[r, 2:], ref, n ** 3, prm["mu"])
+            assert rows[r, 0] == t
+            dt = twin.step(1)
+            assert rows[r, 1] == dt
+            t = twin.t
+        np.testing.assert_array_equal(twin.get_state(), s.get_state())  # the history does not touch the step
+        assert H.hgks_history_read(s.ctx, 16).shape[0] == 0
+        with pytest.raises(H.HgksError):  # would overflow the 16 rows
+            s.step(17)
