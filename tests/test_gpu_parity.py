@@ -190,6 +190,35 @@ def test_step_parity_tgv32_fp32():
         assert abs(D.enstrophy(a, dx) - zb) <= 1e-4 * zb
 
 
+def test_step_parity_tgv128_config2_fp64_and_fp32():
+    """BASELINE config 2: TGV 128^3, FP64 and FP32 on one B200, 10 CFL steps against the FP64 oracle
+    stepped alongside (~30 s of oracle time per step on 16 host cores): normwise (O-19) <= 1e-11 / 1e-4
+    after every step, per-step E_k and enstrophy to the same tolerances, dt to 1e-13 / 1e-6."""
+    n = 128
+    q, dx = inputs.tgv(n)
+    gas = O.make_gas(mu=TGV["mu"])
+    tol = {H.HGKS_FP64: 1e-11, H.HGKS_FP32: 1e-4}
+    dtol = {H.HGKS_FP64: 1e-13, H.HGKS_FP32: 1e-6}
+    worst = {p: 0.0 for p in tol}
+    with _tgv_solver(n, cfl=0.4) as s64, _tgv_solver(n, cfl=0.4, precision=H.HGKS_FP32) as s32:
+        s64.set_state(q)
+        s32.set_state(q)
+        qo = q
+        for k in range(10):
+            qo, h = O.run(gas, qo, dx, 1)
+            ko, zo = D.kinetic_energy(qo), D.enstrophy(qo, dx)
+            for prec, s in ((H.HGKS_FP64, s64), (H.HGKS_FP32, s32)):
+                dt = s.step(1)
+                assert dt == pytest.approx(h[0], rel=dtol[prec]), (prec, k)
+                a = s.get_state()
+                e = D.normwise_error(a, qo).max()
+                worst[prec] = max(worst[prec], e)
+                assert e <= tol[prec], (prec, k, e)
+                assert abs(D.kinetic_energy(a) - ko) <= tol[prec] * ko, (prec, k)
+                assert abs(D.enstrophy(a, dx) - zo) <= tol[prec] * zo, (prec, k)
+    print(f"TGV 128^3 10 steps: worst normwise error fp64 {worst[H.HGKS_FP64]:.2e}, fp32 {worst[H.HGKS_FP32]:.2e}")
+
+
 @pytest.mark.parametrize("precision", [H.HGKS_FP64, H.HGKS_FP32])
 def test_uniform_flow_bitwise(precision):
     # O-P1: every face sees bitwise-identical inputs, so every face flux of a direction is

@@ -192,3 +192,27 @@ def test_channel_inputs_decomposition_independent():
     np.testing.assert_array_equal(full[:, 4:7], part)
     T = (0.4 * (full[4] - 0.5 * (full[1] ** 2 + full[2] ** 2 + full[3] ** 2) / full[0])) / full[0]
     np.testing.assert_allclose(T, CH["T_w"], rtol=1e-13)
+
+
+@pytest.mark.parametrize("vel", [(0.3, 0.0, 0.0), (0.2, -0.7, 0.1), (0.0, 0.0, 0.0)])
+def test_cfl_dt_on_stretched_mesh_closed_form(vel):
+    """O-13 + O-18 (stretched branch of or_cfl_dt): for a UNIFORM state the CFL step has the closed
+    form dt = cfl * min_d min_j w_{d,j} / (|U_d| + c), c = sqrt(gamma p / rho), with the tanh cell
+    widths w_{y,j} computed here from the face map of P:945-956 written out independently."""
+    n = (12, 40, 10)
+    gr = _channel_grid(n)
+    rho, p = 1.3, 0.9
+    q = np.zeros((5, n[2], n[1], n[0]))
+    q[0] = rho
+    for d in range(3):
+        q[1 + d] = rho * vel[d]
+    q[4] = p / 0.4 + 0.5 * rho * sum(v * v for v in vel)
+    c = math.sqrt(1.4 * p / rho)
+    b = 2.0
+    yf = np.array([np.tanh(b * (2.0 * j / n[1] - 1.0)) / np.tanh(b) for j in range(n[1] + 1)])
+    widths = [np.full(n[0], 2 * math.pi / n[0]), np.diff(yf), np.full(n[2], math.pi / n[2])]
+    expect = 0.4 * min(widths[d].min() / (abs(vel[d]) + c) for d in range(3))
+    got = O.cfl_dt(O.make_gas(T_wall=1.0), q, None, 0.4, grid=gr)
+    assert got == pytest.approx(expect, rel=1e-13)
+    # the wall cells are the narrowest: with V = 0 the y term wins only if it beats x and z
+    assert widths[1].min() == pytest.approx(yf[1] - yf[0], rel=1e-14)
