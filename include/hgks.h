@@ -100,16 +100,26 @@ typedef struct {
 
 /* Validate p, allocate device memory, create streams and (nranks > 1) the NCCL communicator, or
  * join the loopback group (group_key; returns once all nranks members have joined).
+ * Defines: the problem of P:185-204 (conservative variables, gamma, K = (5-3gamma)/(gamma-1) P:202),
+ * tau = mu/p with mu(T) (power law and Pr), the CFL time step (Alg. 1
+ * P:419-421), and one domain per process/GPU ("the computational domain is divided into N parts ...
+ * N GPUs are used"; here along z).  Own stream (stream == NULL): a blocking stream that
+ * orders with the legacy default stream.  Walls on both x and y are rejected (HGKS_EINVAL).
  * *out receives the context, or NULL on failure.  Errors: EINVAL, ECUDA, ENCCL (NCCL init failure
  * or loopback group timeout / inconsistent nranks), ENOMEM. */
 int hgks_create(const hgks_params* p, hgks_ctx** out);
 
-/* This rank's slab: global z planes [z_begin, z_begin + nz_local).  Planes are split as evenly as
- * possible, lower ranks taking the remainder (see hgks_slab_of). */
+/* This rank's slab: global z planes [z_begin, z_begin + nz_local) -- the "i-th decomposed
+ * computational domain" of process P_i.  Planes are split as evenly as possible, lower
+ * ranks taking the remainder (see hgks_slab_of).  c, z_begin, nz_local non-NULL (HGKS_EINVAL). */
 int hgks_local_extent(const hgks_ctx* c, int32_t* z_begin, int32_t* nz_local);
 
-/* Copy in this rank's slab q[5][nz_local][ny][nx] (fp64; host pointer, or device pointer when
- * on_device != 0), check validity (rho > 0, p > 0, finite; HGKS_ESTATE names the first bad
+/* Initial data of this rank's domain (the paper's P_0 distributes the divided initial data to each
+ * process; here every rank passes its own part).  Cell averages Q = (rho, rhoU, rhoV,
+ * rhoW, rhoE) of Eq. (2).
+ * Copy in this rank's slab q[5][nz_local][ny][nx] (fp64; host pointer, or device pointer when
+ * on_device != 0; a device buffer must be complete -- the Python binding synchronises torch's
+ * current stream first), check validity (rho > 0, p > 0, finite; HGKS_ESTATE names the first bad
  * global cell) and, in CFL mode, compute the first step's global max wave speed.  q is not
  * retained. */
 int hgks_set_state(hgks_ctx* c, const double* q, int on_device);
@@ -124,11 +134,18 @@ int hgks_set_state(hgks_ctx* c, const double* q, int on_device);
  * On HGKS_ESTATE the state is rolled back to the last good Q^n and *t_inout is that step's start
  * time. */
 int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double* dt_last);
+/* (multi-rank NCCL contexts: the final wait polls ncclCommGetAsyncError; an asynchronous NCCL error,
+ * or no progress for HGKS_NCCL_TIMEOUT_S seconds (environment, default 300), aborts both
+ * communicators and returns HGKS_ENCCL -- the context must then be destroyed.) */
 
-/* Copy out this rank's slab in the set_state layout (fp64; host or device pointer). Synchronises. */
+/* Output of this rank's domain (P_0 collects from every process; here each rank reads
+ * its own part).  Copy out this rank's slab in the set_state layout (fp64; host or device pointer;
+ * the library owns nothing of q).  Errors: HGKS_EINVAL (NULL, no state yet), HGKS_ECUDA, HGKS_ENCCL
+ * (a failed peer, see hgks_step).  Synchronises. */
 int hgks_get_state(hgks_ctx* c, double* q, int on_device);
 
-/* Release everything owned by c.  NULL-safe.  Collective like every call: a loopback-group rank
+/* Release everything owned by c (device buffers, streams, events, NCCL communicators; the end of
+ * the run of Fig. 3's code frame).  NULL-safe.  Collective like every call: a loopback-group rank
  * waits (host barrier) until every rank of the group has entered hgks_destroy, so no rank frees
  * buffers or events a peer is still using. */
 int hgks_destroy(hgks_ctx* c);

@@ -68,6 +68,10 @@ __device__ __forceinline__ int row_consumers(int l2, int Ls) {
   return max(0, hi - lo + 1);
 }
 
+// watchdog of the spin waits (~seconds): a schedule bug traps (the launch fails with an error) instead
+// of hanging the device
+constexpr unsigned RING_SPIN_LIMIT = 1u << 26;
+
 __device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
 __device__ __forceinline__ void st_volatile(int* p, int v) { *(volatile int*)p = v; }
 
@@ -125,7 +129,8 @@ __global__ void __launch_bounds__(32 * RingCfg<T>::NW, 1)
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // first ring row this warp produces for face row F (-1: none)
+  // first real ring row this warp produces for face row F (-1: none); the schedule (tests/ring_schedule.py
+  // models it): face row bb produces the prologue rows l2 < 4 with l2 % L == bb, then row bb + 4
   auto first_prod = [&](long long F) -> int {
     if (F >= nface_rows) return -1;
     const long long j = F / sm.L;
@@ -137,8 +142,8 @@ __global__ void __launch_bounds__(32 * RingCfg<T>::NW, 1)
   };
 
   // ---- t1 pass (A3) of the staged row into ring slot(s): items (a, m, c), 80 per row ----------------
-  // Every stream row is produced exactly once, by the warp of face row l2 - 4 (rows 0..3: face rows
-  // 0..3).  Rows past a ragged strip end (l2 >= Ls + 4) get a NULL production (real = false): no data,
+  // Every stream row is produced exactly once, by the warp of face row l2 - 4 (rows 0..3: face row
+  // l2 % L).  Rows past a ragged strip end (l2 >= Ls + 4) get a NULL production (real = false): no data,
   // but the slot hand-over (wait for the previous occupant's consumers) still happens, so every slot
   // transition is guarded.
   auto produce = [&](long long j, int l2, bool real) {
@@ -151,8 +156,14 @@ __global__ void __launch_bounds__(32 * RingCfg<T>::NW, 1)
       int t10p, t20p, fnp, Lsp;
       sm.decode(blockIdx.x + jp * G, t10p, t20p, fnp, Lsp);
       const int need = row_consumers(l2p, Lsp);
+      // the slot must hold the previous occupant (its producer has run: producers of one slot then run
+      // in stream order, whatever the warps' drift) and every consumer of it must be done
       if (lane == 0) {
-        while (ld_volatile(&done[sl]) < need) __nanosleep(32);
+        unsigned spins = 0;
+        while (ld_volatile(&seq[sl]) != (int)(Rp + 1) || ld_volatile(&done[sl]) < need) {
+          __nanosleep(32);
+          if (++spins > RING_SPIN_LIMIT) __trap();  // schedule bug: fail the launch instead of hanging
+        }
         st_volatile(&done[sl], 0);
       }
       __syncwarp();
@@ -225,11 +236,14 @@ __global__ void __launch_bounds__(32 * RingCfg<T>::NW, 1)
     const int bb = (int)(F - j * sm.L);
     int t10, t20, fn, Ls;
     sm.decode(blockIdx.x + j * G, t10, t20, fn, Ls);
-    // ---- produce: row bb (strip prologue, bb < 4) and row bb + 4 --------------------------------
-    if (bb < 4) {
-      produce(j, bb, true);
-      if (bb < Ls) issue_stage(j, bb + 4);
+    // ---- produce: the strip's prologue rows l2 < 4 with l2 % L == bb, then row bb + 4 ------------
+    bool staged = true;  // the prefetch holds this face row's first real production
+    for (int l2 = bb; l2 < 4; l2 += sm.L) {
+      if (!staged) issue_stage(j, l2);
+      produce(j, l2, true);
+      staged = false;
     }
+    if (bb < Ls && !staged) issue_stage(j, bb + 4);
     produce(j, bb + 4, bb < Ls);
     {  // prefetch the next production of this warp (its staging buffer is free again)
       const int p = first_prod(F + NW);
@@ -240,7 +254,11 @@ __global__ void __launch_bounds__(32 * RingCfg<T>::NW, 1)
     const long long R0 = j * L4 + bb;
     if (lane < 5) {
       const int sl = (int)((R0 + lane) % RING);
-      while (ld_volatile(&seq[sl]) != (int)(R0 + lane + 1)) __nanosleep(20);
+      unsigned spins = 0;
+      while (ld_volatile(&seq[sl]) != (int)(R0 + lane + 1)) {
+        __nanosleep(20);
+        if (++spins > RING_SPIN_LIMIT) __trap();
+      }
       __threadfence_block();
     }
     __syncwarp();
