@@ -345,7 +345,15 @@ struct GpFlux {
     // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
     // (below 1e-20 -- dt/tau > 92, e.g. every low-Mach TGV face -- h changes no Gamma above rounding)
     const T harg = -T(0.5) * dt * rcp(tau);
-    h = (tau > T(0) && harg > T(-46)) ? m_exp(harg) : T(0);
+    const bool need_h = tau > T(0) && harg > T(-46);
+#ifdef __CUDA_ARCH__
+    // warp-uniform skip: at low Mach every lane of a warp has dt/tau > 92 (h = 0), and the exp is
+    // ~25 FP64 instructions per Gauss point
+    h = T(0);
+    if (__any_sync(__activemask(), need_h)) h = need_h ? m_exp(harg) : T(0);
+#else
+    h = need_h ? m_exp(harg) : T(0);
+#endif
     if (HGKS_GSHARE) {
       const T om = T(1) - h;
       const T c13 = om * (T(3) - h) * idt;
@@ -407,7 +415,9 @@ struct GpFlux {
     }
   }
 
-  // F += T(s)(rho ga Z + gb X + gc Y), dF likewise with Gamma' (X, Y already carry rho)
+  // F += T(s)(rho ga Z + gb X + gc Y), dF likewise with Gamma' (X, Y already carry rho); FIRST: the
+  // first contribution (F, dF still zero) is assigned
+  template <bool FIRST = false>
   HD void accumulate(bool eq, T rho, T su, T sv, T sw, const T (&Z)[5], const T (&X)[5], const T (&Y)[5]) {
     T ga, gb, gc, gpa, gpb, gpc;
     gammas(eq, ga, gb, gc, gpa, gpb, gpc);
@@ -417,7 +427,7 @@ struct GpFlux {
     for (int k = 0; k < 5; ++k) d[k] = rpa * Z[k] + gpb * X[k] + gpc * Y[k];
     shift_vec(su, sv, sw, d);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) dF[k] += d[k];
+    for (int k = 0; k < 5; ++k) dF[k] = FIRST ? d[k] : dF[k] + d[k];
     if (NEED_F) {
       const T ra = rho * ga;
       T f[5];
@@ -425,7 +435,7 @@ struct GpFlux {
       for (int k = 0; k < 5; ++k) f[k] = ra * Z[k] + gb * X[k] + gc * Y[k];
       shift_vec(su, sv, sw, f);
 #pragma unroll
-      for (int k = 0; k < 5; ++k) F[k] += f[k];
+      for (int k = 0; k < 5; ++k) F[k] = FIRST ? f[k] : F[k] + f[k];
     }
   }
 
@@ -525,7 +535,10 @@ struct GpFlux {
     // fp32 only: in fp64 the tables and the merged slope raise register pressure (more spills) and
     // measured 0.6 % slower despite 30 fewer FP64 instructions per Gauss point (fp32: +0.9 %).  The
     // Pr-fix variant keeps the generic H (its heat-flux density terms reuse e, f).
-    constexpr bool kHfast = HGKS_HFAST && !PRF && sizeof(T) == 4;
+#ifndef HGKS_HFAST64
+#define HGKS_HFAST64 0
+#endif
+    constexpr bool kHfast = HGKS_HFAST && !PRF && (sizeof(T) == 4 || HGKS_HFAST64);
     // moment tables of this side: sn[n] = (t_{n+2} + k2 t_n)/2, tth[n] = theta t_n, so that
     //   e(al, n) = al0 t_n + al1 t_{n+1} + al4 sn[n],  f(al, n) = e(al, n) + al4 tth[n]
     // (k4 - k2 = 2 theta) and H_n(al) = (e_n, e_{n+1}, al2 tth_n, al3 tth_n, e_{n+2}/2 + (k2/2) f_n)
@@ -631,7 +644,7 @@ struct GpFlux {
       dF[4] += prf * heat(gpa, gpb, gpc);
       if (NEED_F) F[4] += prf * heat(ga, gb, gc);
     }
-    accumulate(false, rho, T(0), V, W, Z, X, Y);
+    accumulate<SIDE == 1 && !PRF>(false, rho, T(0), V, W, Z, X, Y);  // g_l side is the first term
   }
 };
 

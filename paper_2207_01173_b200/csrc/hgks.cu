@@ -23,7 +23,6 @@
 #include "../../include/hgks.h"
 #include "../../include/hgks_test.h"
 #include "hgks_kernels.cuh"
-#include "flux_ring.cuh"
 #include "diag_kernels.cuh"
 
 using namespace hgks;
@@ -491,27 +490,9 @@ static int fill_ghosts(hgks_ctx* c, T* q, bool wait_halo) {
 
 // function attributes belong to the device: kept per context (one device each), not process-wide;
 // also set before a graph capture (no attribute calls while capturing)
-#ifndef HGKS_FLUX_RING
-#define HGKS_FLUX_RING 1  // 1: flux_ring_kernel (warp-pipelined strips), 0: flux_kernel (8x8 tiles, normal march)
-#endif
-#ifndef HGKS_RING_L
-#define HGKS_RING_L 128  // max face rows per strip of flux_ring_kernel
-#endif
-
 template <typename T, int STAGE>
 static int set_flux_attrs(hgks_ctx* c) {
   if (c->flux_attr_set[STAGE - 1]) return HGKS_OK;
-  if (HGKS_FLUX_RING) {
-    const int sr = (int)ring_smem_bytes<T>();
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 2, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    CUDA_TRY(c, cudaFuncSetAttribute(flux_ring_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr));
-    c->flux_attr_set[STAGE - 1] = true;
-    return HGKS_OK;
-  }
   const int sm = (int)flux_smem_bytes<T>();
   CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -613,35 +594,12 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   auto flux = [&](int d) -> int {
     T* ff = ffbuf(d);
     const int n1 = n3[(d + 1) % 3], n2 = n3[(d + 2) % 3];
-    if (HGKS_FLUX_RING) {
-      // strips of TT1 faces x L face rows at one normal face index; one persistent block per SM
-      StripMap sm;
-      sm.n1t = (n1 + TT1 - 1) / TT1;
-      sm.n2c = (n2 + HGKS_RING_L - 1) / HGKS_RING_L;
-      sm.L = (n2 + sm.n2c - 1) / sm.n2c;
-      sm.n2 = n2;
-      const long long nstrips = (long long)sm.n1t * sm.n2c * (n3[d] + 1);
-      const int grid = (int)std::min<long long>(nstrips, c->num_sms);
-      const size_t sr = ring_smem_bytes<T>();
-      const int nt = 32 * RingCfg<T>::NW;
-      CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
-      prof_begin(c, HGKS_K_FLUX_X + d);
-      const bool prf = c->p.prandtl != 1.0;
-      if (d == 0 && !prf) flux_ring_kernel<T, 0, STAGE, false><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, sm, nstrips);
-      if (d == 1 && !prf) flux_ring_kernel<T, 1, STAGE, false><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, sm, nstrips);
-      if (d == 2 && !prf) flux_ring_kernel<T, 2, STAGE, false><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, sm, nstrips);
-      if (d == 0 && prf) flux_ring_kernel<T, 0, STAGE, true><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, sm, nstrips);
-      if (d == 1 && prf) flux_ring_kernel<T, 1, STAGE, true><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, sm, nstrips);
-      if (d == 2 && prf) flux_ring_kernel<T, 2, STAGE, true><<<grid, nt, sr, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, sm, nstrips);
-      prof_end(c, HGKS_K_FLUX_X + d);
-      CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
-      return HGKS_OK;
-    }
     // faces per block along the normal: at most HGKS_FLUX_TPB (measured at 256^3: 16 > 8 > 4 > 2 by
     // 0.4 % / 1 % / 2 %), chosen to balance that against the last partial wave of blocks (thin
     // slabs: 256 x 256 x 32 gives 7.35 waves at 16 faces per block, 14.7 at 8)
+    constexpr int TT2 = FluxCfg<T>::TT2;
     const long long tiles = (long long)((n1 + TT1 - 1) / TT1) * ((n2 + TT2 - 1) / TT2);
-    const double slots = 148.0 * (sizeof(T) == 4 ? HGKS_FLUX_MINB32 : HGKS_FLUX_MINB);
+    const double slots = (double)c->num_sms * FluxCfg<T>::MINB;
     int fpb = HGKS_FLUX_TPB;
     double best = -1.0;
     for (int f = HGKS_FLUX_TPB; f >= 2; f /= 2) {
@@ -657,12 +615,12 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
     const bool prf = c->p.prandtl != 1.0;
-    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
-    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
-    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
-    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
-    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
-    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, NTHREADS_FLUX, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
+    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
+    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
+    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
+    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
+    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
+    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
     prof_end(c, HGKS_K_FLUX_X + d);
     CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
     return HGKS_OK;

@@ -180,27 +180,39 @@ __device__ __forceinline__ void block_sum_warps(double (&v)[N], double* sh) {
 #ifndef HGKS_FLUX_TPB
 #define HGKS_FLUX_TPB 16  // max consecutive normal faces per flux block (host lowers it for small grids)
 #endif
+// Tile shape and residency per precision (measured at TGV 256^3):
+//   fp64: 8 x 4 faces (128 threads), 3 blocks per SM, 168 registers, no spills: +2 % over 8 x 8 faces at 2
+//         blocks per SM (128 registers, spills), although the t1 pass then serves 8 rows per 4 faces
+//   fp32: 8 x 8 faces (256 threads), 3 blocks per SM, 80 registers (8 x 4 at 6 blocks: -10 %)
+#ifndef HGKS_TT2_64
+#define HGKS_TT2_64 4
+#endif
 #ifndef HGKS_FLUX_MINB
-#define HGKS_FLUX_MINB 2  // resident flux blocks per SM (register budget 128/thread)
+#define HGKS_FLUX_MINB 3
+#endif
+#ifndef HGKS_TT2_32
+#define HGKS_TT2_32 8
 #endif
 #ifndef HGKS_FLUX_MINB32
-#define HGKS_FLUX_MINB32 3  // fp32: 54.7 KB shared memory per block, 3 blocks fit; 80 registers, no spills (+1.8 %; 4 blocks spill: -9 %)
+#define HGKS_FLUX_MINB32 3
 #endif
-#ifndef HGKS_TT2
-#define HGKS_TT2 8
-#endif
-constexpr int TT1 = 8, TT2 = HGKS_TT2;      // faces per tile along t1, t2
-constexpr int TL1 = TT1 + 4, TL2 = TT2 + 4;  // lines per tile (+-2 tangential halo)
-constexpr int NTHREADS_FLUX = TT1 * TT2 * 4;
+constexpr int TT1 = 8, TL1 = TT1 + 4;  // faces / lines (+-2 tangential halo) per tile along t1
+template <typename T>
+struct FluxCfg {
+  static constexpr int TT2 = sizeof(T) == 8 ? HGKS_TT2_64 : HGKS_TT2_32;  // faces per tile along t2
+  static constexpr int TL2 = TT2 + 4;                                      // lines along t2
+  static constexpr int NT = TT1 * TT2 * 4;                                 // threads: one per Gauss point
+  static constexpr int MINB = sizeof(T) == 8 ? HGKS_FLUX_MINB : HGKS_FLUX_MINB32;
+  static constexpr int SA_C = TL2 * TL1 + 8;  // one (field, component) plane of sA
+};
 constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
 // shared-memory strides (in elements), padded so that half-warps hit 16 distinct 8-byte banks
-constexpr int SA_C = TL2 * TL1 + 8;          // one (field, component) plane of sA: 152
 constexpr int SB_K = 2 * TT1;                // one slot k of sB: (m, a) = 16
 constexpr int SB_RC = NB * SB_K + 8;         // one (row, component) block of sB: 152
 
 template <typename T>
 constexpr size_t flux_smem_bytes() {
-  return sizeof(T) * (6 * 5 * SA_C + TL2 * 5 * SB_RC);
+  return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::TL2 * 5 * SB_RC);
 }
 
 #ifndef HGKS_CP16
@@ -369,11 +381,12 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
 // Lane layout in phase C: lane = 16 n + 8 m + a (a = t1 face in tile, (m, n) the Gauss point),
 // warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
 template <typename T, int DIR, int STAGE, bool PRF>
-__global__ void __launch_bounds__(NTHREADS_FLUX, sizeof(T) == 4 ? HGKS_FLUX_MINB32 : HGKS_FLUX_MINB)
+__global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl,
                 int fpb) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
+  constexpr int TT2 = FluxCfg<T>::TT2, TL2 = FluxCfg<T>::TL2, NTHREADS_FLUX = FluxCfg<T>::NT, SA_C = FluxCfg<T>::SA_C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sA = reinterpret_cast<T*>(smem_raw);  // [6][5][SA_C]
   T* sB = sA + 6 * 5 * SA_C;               // [TL2][5][SB_RC]
@@ -531,26 +544,42 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, sizeof(T) == 4 ? HGKS_FLUX_MINB
     wvl[r] = (!kRowMirror && nn) ? T(kWV0(4 - r)) : T(kWV0(r));
     wdl[r] = (!kRowMirror && nn) ? -T(kWD0(4 - r)) : T(kWD0(r));
   }
+#ifndef HGKS_TV_FENCE
+#define HGKS_TV_FENCE 1  // keep the t2-pass loads from being hoisted (register pressure)
+#endif
+#ifndef HGKS_TV_SPLIT
+#define HGKS_TV_SPLIT 0  // 1: each 5-tap sum as two partial chains (shorter dependency latency)
+#endif
   auto tv = [&](int c, int k) {
-    asm volatile("" ::: "memory");
+    if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
+    if (HGKS_TV_SPLIT) {
+      const T* p = row0 + c * SB_RC + k * SB_K;
+      const T a0 = (kRowMirror ? wv0<T>(0) : wvl[0]) * p[0] + (kRowMirror ? wv0<T>(2) : wvl[2]) * p[2 * rstep] +
+                   (kRowMirror ? wv0<T>(4) : wvl[4]) * p[4 * rstep];
+      const T a1 = (kRowMirror ? wv0<T>(1) : wvl[1]) * p[rstep] + (kRowMirror ? wv0<T>(3) : wvl[3]) * p[3 * rstep];
+      return a0 + a1;
+    }
     T v = T(0);
 #pragma unroll
     for (int r = 0; r < 5; ++r) v += (kRowMirror ? wv0<T>(r) : wvl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
     return v;
   };
+  // row mirror: the derivative of a mirrored row stream carries the sign sgn, folded into ih2s (every
+  // t2 derivative is multiplied by the metric ih2)
+  const T ih2s = kRowMirror ? sgn * ih2 : ih2;
   auto td = [&](int c, int k) {
-    asm volatile("" ::: "memory");
+    if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
     for (int r = 0; r < 5; ++r) v += (kRowMirror ? wd0<T>(r) : wdl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
-    return kRowMirror ? sgn * v : v;
+    return v;
   };
   const T dt = T(ctl->dt);
   GpFlux<T, STAGE == 1, PRF> gf;
   // value and t2-derivative of Ql, Qr from the same five row loads (the t2 derivatives are held
   // until the side passes: 10 more live registers, 50 fewer shared loads per Gauss point)
   auto tvd = [&](int c, int k, T& v, T& d) {
-    asm volatile("" ::: "memory");
+    if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
     v = T(0);
     d = T(0);
 #pragma unroll
@@ -559,7 +588,6 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, sizeof(T) == 4 ? HGKS_FLUX_MINB
       v += (kRowMirror ? wv0<T>(r) : wvl[r]) * x;
       d += (kRowMirror ? wd0<T>(r) : wdl[r]) * x;
     }
-    if (kRowMirror) d *= sgn;
   };
   T d2l[5], d2r[5];
   {
@@ -573,15 +601,15 @@ __global__ void __launch_bounds__(NTHREADS_FLUX, sizeof(T) == 4 ? HGKS_FLUX_MINB
   }
   gf.template add_side<+1>([&](int i, T (&d)[5]) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 2) : (i == 1 ? tv(c, 6) * ih1 : d2l[c] * ih2);
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 2) : (i == 1 ? tv(c, 6) * ih1 : d2l[c] * ih2s);
   });
   gf.template add_side<-1>([&](int i, T (&d)[5]) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 3) : (i == 1 ? tv(c, 7) * ih1 : d2r[c] * ih2);
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 3) : (i == 1 ? tv(c, 7) * ih1 : d2r[c] * ih2s);
   });
   gf.add_equilibrium([&](int i, T (&d)[5]) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 5) : (i == 1 ? tv(c, 8) * ih1 : td(c, 4) * ih2);
+    for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 5) : (i == 1 ? tv(c, 8) * ih1 : td(c, 4) * ih2s);
   });
   T F[5], dF[5];
 #pragma unroll

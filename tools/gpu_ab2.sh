@@ -3,7 +3,7 @@
 # usage: bash tools/gpu_ab2.sh "<pytest args or empty>" v1 v2 ...   (libhgks_<v>.so; "default" = libhgks.so)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 T="$1"; shift
-if [ -n "$T" ]; then timeout 1200 python -m pytest $T -x -q --timeout 300 > gpurun_out/ab_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ab_pytest.log; tail -3 gpurun_out/ab_pytest.log; fi
+if [ -n "$T" ]; then eval timeout 1200 python -m pytest $T -x -q --timeout 300 > gpurun_out/ab_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ab_pytest.log; tail -3 gpurun_out/ab_pytest.log; fi
 for v in "$@"; do
   if [ "$v" = default ]; then L=$PWD/paper_2207_01173_b200/libhgks.so; else L=$PWD/paper_2207_01173_b200/libhgks_$v.so; fi
   for args in "" "--weak"; do

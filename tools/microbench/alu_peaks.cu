@@ -18,6 +18,40 @@ __global__ void fma_loop(T* out, int iters, T seed) {
   if (acc == T(12345.678)) out[0] = acc;
 }
 
+// packed FP32 (FFMA2): 8 independent float2 chains per thread
+__global__ void ffma2_loop(float* out, int iters, float seed) {
+  float2 x[8];
+  for (int k = 0; k < 8; ++k) x[k] = make_float2(seed + k + threadIdx.x, seed - k);
+  const float2 a = make_float2(0.999999f, 0.999998f), b = make_float2(1e-7f, 2e-7f);
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __ffma2_rn(x[k], a, b);
+  float acc = 0.f;
+  for (int k = 0; k < 8; ++k) acc += x[k].x + x[k].y;
+  if (acc == 12345.678f) out[0] = acc;
+}
+
+static double ffma2_tflops(int blocks, int threads, int iters) {
+  float* out;
+  cudaMalloc(&out, sizeof(float));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    ffma2_loop<<<blocks, threads>>>(out, iters, 1.f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = (double)blocks * threads * iters * 8 * 4;
+    if (rep > 0 && fl / ms / 1e9 > best) best = fl / ms / 1e9;
+  }
+  cudaFree(out);
+  return best;
+}
+
 template <typename T>
 static double tflops(int blocks, int threads, int iters) {
   T* out;
@@ -46,8 +80,9 @@ int main() {
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
   const double d = tflops<double>(sms * 4, 256, 20000);
   const double f = tflops<float>(sms * 4, 256, 40000);
-  printf("{\"dfma_tflops\": %.3f, \"ffma_tflops\": %.3f, \"sms\": %d, \"clock_rate_mhz_attr\": %.0f, "
+  const double f2 = ffma2_tflops(sms * 4, 256, 20000);
+  printf("{\"dfma_tflops\": %.3f, \"ffma_tflops\": %.3f, \"ffma2_tflops\": %.3f, \"sms\": %d, \"clock_rate_mhz_attr\": %.0f, "
          "\"how\": \"tools/microbench/alu_peaks.cu: 8 independent FMA chains per thread, %d blocks x 256, best of 4\"}\n",
-         d, f, sms, clk_khz / 1000.0, sms * 4);
+         d, f, f2, sms, clk_khz / 1000.0, sms * 4);
   return 0;
 }
