@@ -360,6 +360,22 @@ def measure_rank(args, env) -> dict | None:
             a1.record(stream)
             torch.cuda.synchronize(env.device)
             aux[name + "_ms"] = a0.elapsed_time(a1) / 3
+        # per-step diagnostic history (fused into the stage-1 update): cost per step, 4 steps with and without
+        def timed_steps(k):
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            env.barrier()
+            b0.record(stream)
+            s.step(k)
+            b1.record(stream)
+            env.barrier()
+            return env.reduce(b0.elapsed_time(b1), "max") / k
+        t_off = timed_steps(4)
+        H.hgks_history_enable(s.ctx, 8)
+        t_on = timed_steps(4)
+        hist = H.hgks_history_read(s.ctx, 8)
+        H.hgks_history_enable(s.ctx, 0)
+        aux["history_ms_per_step"] = t_on - t_off
+        aux["history_rows_read"] = int(hist.shape[0])
         res["aux"] = aux
         # e2e through the public API with host buffers (pinned): H2D state, step, D2H state per step
         if not args.no_e2e:
