@@ -325,6 +325,9 @@ def measure_rank(args, env) -> dict | None:
         if (prec_name == "fp32" and args.no_fp32) or (prec_name == "fp64" and args.only_fp32):
             continue
         s = make_solver(prec)
+        if ws > 1:  # evidence of the N-rank launch for the driver's log (stderr; stdout is the JSON line)
+            print(f"[bench] {prec_name}: rank {rank}/{ws} on cuda:{env.device}, transport {env.transport}, "
+                  f"z-slab [{s.z0}, {s.z0 + s.nz_local}) of {grid[2]}", file=sys.stderr, flush=True)
         q = local_field(s)
         with torch.cuda.device(env.device):
             qd = torch.from_numpy(q).cuda()

@@ -258,11 +258,6 @@ __device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
   return L;
 }
 
-#ifndef HGKS_RC_PF
-#define HGKS_RC_PF 4  // cells of the reconstruction march prefetched ahead (1: none)
-#endif
-constexpr int RC_PF = HGKS_RC_PF;
-
 // Subset of the face lines of one sweep: lines lbeg + j for j in [0, lcnt), where j >= gap_at
 // skips ahead by gap (two disjoint ranges in one launch: the ghost-plane lines of the x sweep).
 struct LineRange {
@@ -304,16 +299,8 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
   T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
   T Ap = T(0), Bp = T(0);  // edges of cell fn-1
-  // software prefetch: the next RC_PF cells of the march are in flight while cell fn is reconstructed
-  // (window index fn + 5 of the march ends at fe + 4, the last ghost layer)
-  T pf[RC_PF];
-#pragma unroll
-  for (int k = 0; k < RC_PF; ++k) pf[k] = (fs + 4 + k <= fe + 4) ? p[(fs + 4 + k) * sN] : T(0);
   for (int fn = fs - 1; fn < fe; ++fn) {
-    s5 = pf[0];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
-#pragma unroll
-    for (int k = 0; k + 1 < RC_PF; ++k) pf[k] = pf[k + 1];
-    pf[RC_PF - 1] = (fn + 5 + RC_PF <= fe + 4) ? p[(fn + 5 + RC_PF) * sN] : T(0);
+    s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
     if (fn >= fs) {
@@ -363,14 +350,8 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
   const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
   T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
   T Ap = T(0), Bp = T(0);
-  T pf[RC_PF];  // software prefetch, as recon_kernel
-#pragma unroll
-  for (int k = 0; k < RC_PF; ++k) pf[k] = (fs + 4 + k <= fe + 4) ? p[(fs + 4 + k) * sN] : T(0);
   for (int fn = fs - 1; fn < fe; ++fn) {
-    s5 = pf[0];
-#pragma unroll
-    for (int k = 0; k + 1 < RC_PF; ++k) pf[k] = pf[k + 1];
-    pf[RC_PF - 1] = (fn + 5 + RC_PF <= fe + 4) ? p[(fn + 5 + RC_PF) * sN] : T(0);
+    s5 = p[(fn + 5) * sN];
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);
     if (fn >= fs) {
