@@ -33,6 +33,25 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+FLOPCOUNT_SRC = os.path.join(HERE, "flopcount.cpp")
+FLOPCOUNT_BIN = os.path.join(HERE, "flopcount")
+
+
+def build_flopcount(force: bool = False) -> str:
+    """g++ the counting build of the oracle (oracle/flopcount.cpp: hgks_oracle.c with a counting double)."""
+    if force or not os.path.exists(FLOPCOUNT_BIN) or os.path.getmtime(FLOPCOUNT_BIN) < max(
+        os.path.getmtime(FLOPCOUNT_SRC), os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "hgks_oracle.h"))
+    ):
+        subprocess.check_call(["g++", "-O1", "-std=c++17", "-w", "-o", FLOPCOUNT_BIN, FLOPCOUNT_SRC])
+    return FLOPCOUNT_BIN
+
+
+def flopcount() -> dict:
+    """The oracle's arithmetic counted on TGV 16^3 (flops per Gauss point, face, cell-update)."""
+    import json
+    return json.loads(subprocess.check_output([build_flopcount()]))
+
+
 class Gas(C.Structure):
     _fields_ = [("gamma", C.c_double), ("K", C.c_double), ("prandtl", C.c_double),
                 ("mu_law", C.c_int), ("mu_ref", C.c_double), ("T_ref", C.c_double),
