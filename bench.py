@@ -363,18 +363,17 @@ def measure_rank(args, env) -> dict | None:
             a1.record(stream)
             torch.cuda.synchronize(env.device)
             aux[name + "_ms"] = a0.elapsed_time(a1) / 3
-        # per-step diagnostic history (fused into the stage-1 update): cost per step, 4 steps with and without
-        def timed_steps(k):
-            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            env.barrier()
-            b0.record(stream)
+        # per-step diagnostic history (fused into the stage-1 update): its cost per step is the growth of the
+        # update-class event time (the fused diagnostics + the two reduction kernels), 6 steps each way
+        def update_ms(k):
+            H.hgks_profile_enable(s.ctx, True)
             s.step(k)
-            b1.record(stream)
-            env.barrier()
-            return env.reduce(b0.elapsed_time(b1), "max") / k
-        t_off = timed_steps(4)
+            ms_k2, _, _ = H.hgks_profile_read(s.ctx)
+            H.hgks_profile_enable(s.ctx, False)
+            return env.reduce(ms_k2["update"], "max") / k
+        t_off = update_ms(6)
         H.hgks_history_enable(s.ctx, 8)
-        t_on = timed_steps(4)
+        t_on = update_ms(6)
         hist = H.hgks_history_read(s.ctx, 8)
         H.hgks_history_enable(s.ctx, 0)
         aux["history_ms_per_step"] = t_on - t_off

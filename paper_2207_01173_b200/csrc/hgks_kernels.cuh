@@ -104,35 +104,18 @@ __device__ __forceinline__ long long qidx(const Geo<T>& g, int v, int i, int j, 
 // either precision.  Used by diag_kernel (on demand) and by the stage-1 update (per-step history).
 constexpr int NDIAG = 11;  // HGKS_DIAG_COUNT
 
+// velocity (U, V, W) of one cell in fp64: one reciprocal of rho (MUFU seed + Newton, ~1 ulp) per cell
+// instead of three IEEE divisions
 template <typename T>
-__device__ __forceinline__ double vel_of(const T* __restrict__ q, const Geo<T>& g, int c, int i, int j, int k) {
-  return (double)q[qidx(g, 1 + c, i, j, k)] / (double)q[qidx(g, 0, i, j, k)];
+__device__ __forceinline__ void vel_of(const T* __restrict__ q, const Geo<T>& g, int i, int j, int k, double (&u)[3]) {
+  const double ir = rcp((double)q[qidx(g, 0, i, j, k)]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) u[c] = (double)q[qidx(g, 1 + c, i, j, k)] * ir;
 }
 
-template <typename T>
-__device__ __forceinline__ void diag_cell(const T* __restrict__ q, const Geo<T>& g, const DiagGeo& dg, double gamma, int i,
-                                          int j, int k, double (&acc)[NDIAG]) {
-  const int ijk[3] = {i, j, k};
-  const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
-  const double rho = (double)q[qidx(g, 0, i, j, k)];
-  double u[3], m[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    m[c] = (double)q[qidx(g, 1 + c, i, j, k)];
-    u[c] = m[c] / rho;
-  }
-  double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25)
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double J = dg.jc[d][ijk[d]];
-    const int di = d == 0, dj = d == 1, dk = d == 2;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double d1 = vel_of(q, g, c, i + di, j + dj, k + dk) - vel_of(q, g, c, i - di, j - dj, k - dk);
-      const double d2 = vel_of(q, g, c, i + 2 * di, j + 2 * dj, k + 2 * dk) - vel_of(q, g, c, i - 2 * di, j - 2 * dj, k - 2 * dk);
-      grad[c][d] = J * (8.0 * d1 - d2) / 12.0;
-    }
-  }
+// the per-cell integrands from the cell's state and velocity gradient
+__device__ __forceinline__ void diag_terms(double rho, const double (&u)[3], const double (&m)[3], const double (&grad)[3][3],
+                                           double rhoE, double vol, double gamma, double (&acc)[NDIAG]) {
   const double o0 = grad[2][1] - grad[1][2], o1 = grad[0][2] - grad[2][0], o2 = grad[1][0] - grad[0][1];
   const double om2 = o0 * o0 + o1 * o1 + o2 * o2;
   const double dv = grad[0][0] + grad[1][1] + grad[2][2];
@@ -145,11 +128,39 @@ __device__ __forceinline__ void diag_cell(const T* __restrict__ q, const Geo<T>&
   acc[5] += m[0] * vol;
   acc[6] += m[1] * vol;
   acc[7] += m[2] * vol;
-  const double rhoE = (double)q[qidx(g, 4, i, j, k)];
   acc[8] += rhoE * vol;
   acc[9] += vol;
   const double p = (gamma - 1.0) * (rhoE - 0.5 * rho * u2);
   acc[10] += p * dv * vol;  // pressure-dilatation (O-29)
+}
+
+template <typename T>
+__device__ __forceinline__ void diag_cell(const T* __restrict__ q, const Geo<T>& g, const DiagGeo& dg, double gamma, int i,
+                                          int j, int k, double (&acc)[NDIAG]) {
+  const int ijk[3] = {i, j, k};
+  const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
+  const double rho = (double)q[qidx(g, 0, i, j, k)];
+  double u[3], m[3];
+  const double ir = rcp(rho);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    m[c] = (double)q[qidx(g, 1 + c, i, j, k)];
+    u[c] = m[c] * ir;
+  }
+  double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25)
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double J12 = dg.jc[d][ijk[d]] * (1.0 / 12.0);
+    const int di = d == 0, dj = d == 1, dk = d == 2;
+    double up1[3], um1[3], up2[3], um2[3];
+    vel_of(q, g, i + di, j + dj, k + dk, up1);
+    vel_of(q, g, i - di, j - dj, k - dk, um1);
+    vel_of(q, g, i + 2 * di, j + 2 * dj, k + 2 * dk, up2);
+    vel_of(q, g, i - 2 * di, j - 2 * dj, k - 2 * dk, um2);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) grad[c][d] = J12 * (8.0 * (up1[c] - um1[c]) - (up2[c] - um2[c]));
+  }
+  diag_terms(rho, u, m, grad, (double)q[qidx(g, 4, i, j, k)], vol, gamma, acc);
 }
 
 // sum v[0..N) over a DIAG_TPB block in a fixed order (warp butterflies, then the warps in order);
@@ -850,7 +861,46 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
     double acc[NDIAG];
 #pragma unroll
     for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
-    if (i < nx && j < ny) diag_cell(Q, g, dg, gamma, i, j, k, acc);
+    // velocities of the block's 64 x 4 cells and their +-2 x/y halo, one reciprocal each, staged in
+    // shared memory; the z neighbours (other planes) come from global memory
+    constexpr int TX = UPD_X + 4, TY = UPD_Y + 4;
+    __shared__ double su[3][TY][TX];
+    for (int e = threadIdx.x; e < TX * TY; e += DIAG_TPB) {
+      const int lx = e % TX, ly = e / TX;
+      const int gi = blockIdx.x * UPD_X + lx - 2, gj = blockIdx.y * UPD_Y + ly - 2;
+      if (gi <= nx + 2 && gj <= ny + 2) {
+        double uu[3];
+        vel_of(Q, g, gi, gj, k, uu);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) su[c][ly][lx] = uu[c];
+      }
+    }
+    __syncthreads();
+    if (i < nx && j < ny) {
+      const int lx = threadIdx.x % UPD_X + 2, ly = threadIdx.x / UPD_X + 2;
+      const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
+      const double rho = (double)Q[qidx(g, 0, i, j, k)];
+      double u[3], m[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        m[c] = (double)Q[qidx(g, 1 + c, i, j, k)];
+        u[c] = su[c][ly][lx];
+      }
+      double grad[3][3];  // grad[c][d] = d u_c / d x_d (O-25), as diag_cell
+      double up1[3], um1[3], up2[3], um2[3];
+      vel_of(Q, g, i, j, k + 1, up1);
+      vel_of(Q, g, i, j, k - 1, um1);
+      vel_of(Q, g, i, j, k + 2, up2);
+      vel_of(Q, g, i, j, k - 2, um2);
+      const double Jx = dg.jc[0][i] * (1.0 / 12.0), Jy = dg.jc[1][j] * (1.0 / 12.0), Jz = dg.jc[2][k] * (1.0 / 12.0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        grad[c][0] = Jx * (8.0 * (su[c][ly][lx + 1] - su[c][ly][lx - 1]) - (su[c][ly][lx + 2] - su[c][ly][lx - 2]));
+        grad[c][1] = Jy * (8.0 * (su[c][ly + 1][lx] - su[c][ly - 1][lx]) - (su[c][ly + 2][lx] - su[c][ly - 2][lx]));
+        grad[c][2] = Jz * (8.0 * (up1[c] - um1[c]) - (up2[c] - um2[c]));
+      }
+      diag_terms(rho, u, m, grad, (double)Q[qidx(g, 4, i, j, k)], vol, gamma, acc);
+    }
     __shared__ double shd[NDIAG * (DIAG_TPB / 32)];
     block_sum_warps(acc, shd);
     if (threadIdx.x == 0) {
