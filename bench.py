@@ -14,6 +14,8 @@ Launch modes (one JSON line from rank 0 in every mode):
                                            visible GPUs round-robin (the in-process loopback group of
                                            hgks.h: same kernels, slab split, halo plan and collectives'
                                            placement as NCCL) -- a dry run of the N-rank path on 1 GPU
+  python bench.py --transport nccl-self    1 rank through a one-member NCCL communicator (halo by NCCL
+                                           self send/recv, NCCL allreduce): the NCCL calls on 1 GPU
   python bench.py --impl reference         the plain CPU oracle on the host cores (reference arm)
 
 Prints ONE JSON line on rank 0 (DESIGN.md §8 "Measurement").
@@ -212,9 +214,10 @@ def run_reference(args):
 class NcclEnv:
     transport = "nccl"
 
-    def __init__(self, dist, ws, rank, local):
+    def __init__(self, dist, ws, rank, local, self_comm=False):
         import torch
         self.dist, self.ws, self.rank, self.device = dist, ws, rank, local
+        self.self_comm = self_comm  # one rank, NCCL transport anyway (--transport nccl-self)
         self.stream = torch.cuda.Stream(device=local)
 
     def barrier(self):
@@ -233,9 +236,9 @@ class NcclEnv:
 
     def comm_kwargs(self):
         """A FRESH NCCL unique id for every context (NCCL's bootstrap root serves one init)."""
-        if self.ws == 1:
-            return {}
         from paper_2207_01173_b200 import hgks as H
+        if self.ws == 1:
+            return {"nccl_id": H.hgks_get_nccl_id()} if self.self_comm else {}
         obj = [H.hgks_get_nccl_id() if self.rank == 0 else None]
         self.dist.broadcast_object_list(obj, src=0)
         return {"nccl_id": obj[0]}
@@ -493,8 +496,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hgks", choices=["hgks", "reference"])
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "loopback"],
-                    help="nccl: one process per GPU; loopback: N ranks in this process (one GPU suffices)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "loopback", "nccl-self"],
+                    help="nccl: one process per GPU; loopback: N ranks in this process (one GPU suffices); "
+                         "nccl-self: one rank with a one-member NCCL communicator (the z halo as NCCL self "
+                         "send/recv, the CFL word by NCCL allreduce): the NCCL code path on one GPU")
     ap.add_argument("--n", type=int, default=256, help="TGV grid n^3 (BASELINE config 3: 256)")
     ap.add_argument("--workload", default="tgv", choices=["tgv", "channel"],
                     help="tgv: config 3 (headline); channel: config 4 (H2 128x256x128 unless --channel-grid)")
@@ -509,6 +514,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    if args.transport == "nccl-self" and args.gpus != 1:
+        raise SystemExit("bench.py: --transport nccl-self is a one-rank run (--gpus 1)")
     if args.transport == "nccl" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # the driver launches N > 1 under torch.distributed.run; a bare `--gpus N` re-executes so
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
@@ -550,9 +557,10 @@ def main():
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    out = measure_rank(args, NcclEnv(dist, ws, rank, local))
+    out = measure_rank(args, NcclEnv(dist, ws, rank, local, self_comm=args.transport == "nccl-self"))
     if out is not None:
-        report(args, out, ws, "nccl" if ws > 1 else "none (1 rank)")
+        report(args, out, ws, "nccl" if ws > 1 else ("nccl (one-member communicator)" if args.transport == "nccl-self"
+                                                      else "none (1 rank)"))
     if ws > 1:
         dist.destroy_process_group()
 

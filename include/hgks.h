@@ -82,7 +82,12 @@ typedef struct {
   hgks_precision precision;
   int32_t rank, nranks;  /* slab decomposition along z (outermost storage axis)                   */
   int32_t device;        /* CUDA device ordinal used by this context                              */
-  const void* nccl_id;   /* 128-byte ncclUniqueId identical on all ranks; NULL iff nranks == 1     */
+  const void* nccl_id;   /* 128-byte ncclUniqueId identical on all ranks; required for NCCL ranks
+                            (nranks > 1, group_key == 0).  With nranks == 1 it is optional: non-NULL
+                            creates a one-member communicator, and the periodic z wrap then runs as
+                            an NCCL self send/recv and every reduction as an NCCL allreduce (the same
+                            calls as P > 1, so the NCCL path can be exercised on one GPU); NULL uses
+                            device copies                                                         */
   void* stream;          /* cudaStream_t for all work; NULL => the library creates one            */
   hgks_force_mode force_mode; /* streamwise body force (see hgks_force_mode); NONE for TGV           */
   double force;          /* CONST: the acceleration f; BULK: f before the first step (f_init)      */

@@ -340,8 +340,7 @@ static int lb_barrier(hgks_ctx* c) {
 
 // in-place allreduce of count elements of buf (device) on stream c->s; op 0: max u64, 1: sum f64
 static int coll_allreduce(hgks_ctx* c, void* buf, size_t count, int op) {
-  if (c->p.nranks == 1) return HGKS_OK;
-  if (c->comm) {
+  if (c->comm) {  // NCCL (also a one-rank communicator, see hgks_create)
     NCCL_TRY(c, ncclAllReduce(buf, buf, count, op == 0 ? ncclUint64 : ncclFloat64, op == 0 ? ncclMax : ncclSum, c->comm, c->s));
     return HGKS_OK;
   }
@@ -374,10 +373,10 @@ static int coll_halo(hgks_ctx* c, void* q, size_t esz) {
   const hgks_halo_plan& pl = c->plan;
   char* b = (char*)q;
   const size_t bytes = (size_t)pl.count * esz;
-  if (c->p.nranks == 1) {  // periodic wrap within the slab
+  if (c->p.nranks == 1 && !c->comm) {  // periodic wrap within the slab
     CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_down * esz, b + pl.send_up * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
     CUDA_TRY(c, cudaMemcpyAsync(b + pl.recv_up * esz, b + pl.send_down * esz, bytes, cudaMemcpyDeviceToDevice, c->sc));
-  } else if (c->comm) {  // one grouped send/recv per neighbour (Alg. 2; O-22: no ordering needed)
+  } else if (c->comm) {  // (one rank: up == down == self, NCCL's self send/recv does the periodic wrap)  // one grouped send/recv per neighbour (Alg. 2; O-22: no ordering needed)
     ncclDataType_t ty = esz == 8 ? ncclFloat64 : ncclFloat32;
     NCCL_TRY(c, ncclGroupStart());
     NCCL_TRY(c, ncclSend(b + pl.send_up * esz, pl.count, ty, pl.up, c->comm_halo, c->sc));
@@ -730,7 +729,7 @@ static int run_steps(hgks_ctx* c, int nsteps) {
 // profiling off only (NCCL and loopback collectives stay on the plain path); HGKS_GRAPHS=0 disables.
 template <typename T>
 static int run_steps_graphed(hgks_ctx* c, int nsteps) {
-  if (!c->graphs || c->prof.on || c->p.nranks != 1 || nsteps < 2) return run_steps<T>(c, nsteps);
+  if (!c->graphs || c->prof.on || c->p.nranks != 1 || c->comm || nsteps < 2) return run_steps<T>(c, nsteps);
   const int par = c->cur;
   int rc;
   if (!c->gexec[par]) {
@@ -975,7 +974,7 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
   if (p->nranks > 1 && p->group_key != 0) {
     int rc = lb_join(c);
     if (rc) return bail(rc);
-  } else if (p->nranks > 1) {
+  } else if (p->nccl_id) {  // nranks >= 1: with one rank a one-member communicator (self send/recv)
     ncclUniqueId id;
     memcpy(&id, p->nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, p->nranks, id, p->rank);

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--precision", type=int, default=H.HGKS_FP64)
+    ap.add_argument("--self-comm", action="store_true", help="one rank: pass an id anyway (one-member communicator)")
     a = ap.parse_args()
     rank, ws, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -31,6 +32,8 @@ def main():
     for leg in range(2):  # two contexts in a row: each needs its own unique id (bootstrap serves one init)
         obj = [H.hgks_get_nccl_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
+        if ws == 1 and not a.self_comm:
+            obj = [None]
         s = H.Solver(grid, (0.0,) * 3, (2 * math.pi,) * 3, mu=2e-3, cfl=0.4, precision=a.precision, rank=rank,
                      nranks=ws, device=local, nccl_id=obj[0])
         s.set_state(np.ascontiguousarray(q[:, s.z0:s.z0 + s.nz_local]))

@@ -64,3 +64,60 @@ def test_bench_loopback_two_ranks():
     assert line["n_gpus"] == 2 and line["config"]["transport"] == "loopback"
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert line["fp32"]["value"] > 0
+
+
+@pytest.mark.parametrize("precision", [H.HGKS_FP64, H.HGKS_FP32])
+def test_nccl_one_member_communicator_bitwise(precision):
+    """The NCCL transport on ONE GPU: a context given an NCCL unique id with nranks = 1 creates a
+    one-member communicator (ncclCommInitRank + ncclCommSplit), runs each stage's periodic z wrap
+    as a grouped NCCL self send/recv on the communication stream and the CFL word / diagnostics as
+    NCCL allreduces -- the calls of coll_halo / coll_allreduce that P > 1 uses.  It must reproduce
+    the device-copy path bitwise (3 CFL steps, state, times and diagnostics), for two contexts in a
+    row (each with a fresh id)."""
+    grid = (20, 18, 23)
+    q, _ = inputs.perturbed(grid, seed=5, amp=0.08)
+    kw = dict(mu=2e-3, cfl=0.4, precision=precision, device=0)
+    with H.Solver(grid, (0.0,) * 3, (2 * math.pi,) * 3, **kw) as s:
+        s.set_state(q)
+        s.step(3)
+        ref, t_ref, d_ref = s.get_state(), s.t, s.diagnostics()
+    for _ in range(2):
+        with H.Solver(grid, (0.0,) * 3, (2 * math.pi,) * 3, nccl_id=H.hgks_get_nccl_id(), **kw) as s:
+            s.set_state(q)
+            s.step(3)
+            got, t_got, d_got = s.get_state(), s.t, s.diagnostics()
+        assert t_got == t_ref
+        assert np.array_equal(got, ref), np.abs(got - ref).max()
+        for k in H.DIAG_NAMES:
+            assert d_got[k] == d_ref[k], (k, d_got[k], d_ref[k])
+
+
+def test_nccl_worker_one_rank_torchrun(tmp_path):
+    """tests/nccl_worker.py (the multi-rank NCCL test's worker: torch.distributed bootstrap, fresh id
+    per context broadcast from rank 0, gather) under torch.distributed.run with ONE rank, which
+    takes the one-member-communicator path: bitwise equal to the plain single-domain run."""
+    out = tmp_path / "nccl1.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "nccl_worker.py"),
+           "--out", str(out), "--precision", str(H.HGKS_FP64), "--self-comm"]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    got = np.load(out)
+    grid = (20, 18, 23)
+    q, _ = inputs.perturbed(grid, seed=5, amp=0.08)
+    with H.Solver(grid, (0.0,) * 3, (2 * math.pi,) * 3, mu=2e-3, cfl=0.4, device=0) as s:
+        s.set_state(q)
+        s.step(3)
+        ref = s.get_state()
+    assert np.array_equal(got["state"], ref) and np.array_equal(got["state_leg2"], ref)
+
+
+def test_bench_nccl_self():
+    """`bench.py --transport nccl-self` (one rank, one-member NCCL communicator) prints one line."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--transport", "nccl-self", "--n", "64",
+           "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e"]
+    r = subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, capture_output=True, text=True)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 1 and line["config"]["transport"].startswith("nccl")
+    assert line["value"] > 0 and line["fp32"]["value"] > 0
