@@ -344,6 +344,7 @@ static int coll_allreduce(hgks_ctx* c, void* buf, size_t count, int op) {
     NCCL_TRY(c, ncclAllReduce(buf, buf, count, op == 0 ? ncclUint64 : ncclFloat64, op == 0 ? ncclMax : ncclSum, c->comm, c->s));
     return HGKS_OK;
   }
+  if (c->p.nranks == 1) return HGKS_OK;
   LoopGroup* G = c->grp;
   const int r = c->p.rank, n = c->p.nranks;
   int rc;
@@ -596,7 +597,7 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     // faces per block along the normal: at most HGKS_FLUX_TPB (measured at 256^3: 16 > 8 > 4 > 2 by
     // 0.4 % / 1 % / 2 %), chosen to balance that against the last partial wave of blocks (thin
     // slabs: 256 x 256 x 32 gives 7.35 waves at 16 faces per block, 14.7 at 8)
-    constexpr int TT2 = FluxCfg<T>::TT2;
+    constexpr int TT1 = FluxCfg<T>::TT1, TT2 = FluxCfg<T>::TT2;
     const long long tiles = (long long)((n1 + TT1 - 1) / TT1) * ((n2 + TT2 - 1) / TT2);
     const double slots = (double)c->num_sms * FluxCfg<T>::MINB;
     int fpb = HGKS_FLUX_TPB;

@@ -3,7 +3,8 @@
 //   recon_kernel<T, 0/2>,       normal reconstruction (A2): one thread per (face line, component,
 //   recon_yz_kernel<T>          march segment), WENO5-Z edges once per cell, six face fields per face
 //                               written to the face-field array of the sweep
-//   flux_kernel<T, DIR, STAGE>  fused per tile of 8x8 faces, marching up to 16 normal faces: 16-byte
+//   flux_kernel<T, DIR, STAGE>  fused per tile of TT1 x TT2 faces (FluxCfg: fp64 4x8, fp32 8x8),
+//                               marching up to 16 normal faces: 16-byte
 //                               cp.async copy of the face fields (A) -> tangential pass t1 (B, A3) ->
 //                               per-Gauss-point thread: tangential pass t2 + BGK flux (C, A4-A6) ->
 //                               4-point face quadrature by warp shuffles (A7) -> face-flux array
@@ -192,11 +193,16 @@ __device__ __forceinline__ void block_sum_warps(double (&v)[N], double* sh) {
 #define HGKS_FLUX_TPB 16  // max consecutive normal faces per flux block (host lowers it for small grids)
 #endif
 // Tile shape and residency per precision (measured at TGV 256^3):
-//   fp64: 8 x 4 faces (128 threads), 3 blocks per SM, 168 registers, no spills: +2 % over 8 x 8 faces at 2
-//         blocks per SM (128 registers, spills), although the t1 pass then serves 8 rows per 4 faces
+//   fp64: 4 x 8 faces (t1 x t2, 128 threads), 3 blocks per SM, no spills.  The t1 pass (phase B) runs
+//         over the TT1 x (TT2 + 4) (face, row) pairs, so the short side goes along t1: 4 x 12 = 48 pairs
+//         per component instead of 8 x 8 = 64 for the 8 x 4 tile (round 2a), 2 passes of 128 threads
+//         instead of 2.5
 //   fp32: 8 x 8 faces (256 threads), 3 blocks per SM, 80 registers (8 x 4 at 6 blocks: -10 %)
+#ifndef HGKS_TT1_64
+#define HGKS_TT1_64 4
+#endif
 #ifndef HGKS_TT2_64
-#define HGKS_TT2_64 4
+#define HGKS_TT2_64 8
 #endif
 #ifndef HGKS_FLUX_MINB
 #define HGKS_FLUX_MINB 3
@@ -207,23 +213,32 @@ __device__ __forceinline__ void block_sum_warps(double (&v)[N], double* sh) {
 #ifndef HGKS_FLUX_MINB32
 #define HGKS_FLUX_MINB32 3
 #endif
-constexpr int TT1 = 8, TL1 = TT1 + 4;  // faces / lines (+-2 tangential halo) per tile along t1
+constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
 template <typename T>
 struct FluxCfg {
-  static constexpr int TT2 = sizeof(T) == 8 ? HGKS_TT2_64 : HGKS_TT2_32;  // faces per tile along t2
-  static constexpr int TL2 = TT2 + 4;                                      // lines along t2
-  static constexpr int NT = TT1 * TT2 * 4;                                 // threads: one per Gauss point
+  static constexpr int TT1 = sizeof(T) == 8 ? HGKS_TT1_64 : 8;                  // faces per tile along t1
+  static constexpr int TL1 = TT1 + 4;                                         // lines (+-2 halo) along t1
+  static constexpr int TT2 = sizeof(T) == 8 ? HGKS_TT2_64 : HGKS_TT2_32;      // faces per tile along t2
+  static constexpr int TL2 = TT2 + 4;                                         // lines along t2
+  static constexpr int NT = TT1 * TT2 * 4;                                    // threads: one per Gauss point
   static constexpr int MINB = sizeof(T) == 8 ? HGKS_FLUX_MINB : HGKS_FLUX_MINB32;
-  static constexpr int SA_C = TL2 * TL1 + 8;  // one (field, component) plane of sA
+  // sA row pitch: TT1 = 4 -> 12 (phase-B half-warps read 4 rows of 4 lines: rows 12 apart hit 4
+  // disjoint 4-bank groups); TT1 = 8 -> TL1 = 12
+  static constexpr int TL1P = TL1 < 12 ? 12 : TL1;
+  static constexpr int SA_C = TL2 * TL1P + 8;  // one (field, component) plane of sA
+  // sB: [TL2 rows][5 comps][SB_RC], slot k of a (row, comp) holds (m, a) = 2 TT1 words.  Pad so that
+  // the phase-C half-warps are conflict-free: TT1 = 8: 16 (m, a) words of one row; TT1 = 4: 8 words
+  // of each of two rows b, b+1, which are 5 SB_RC = 8 (mod 16) 8-byte words apart
+  static constexpr int SB_K = 2 * TT1;
+  static constexpr int SB_RC = TT1 == 8 ? NB * SB_K + 8 : NB * SB_K;  // 152 / 72
+  static constexpr int BPW = 16 / (2 * TT1);  // t2 faces per warp (lane = 16 n + 2 TT1 bl + TT1 m + a)
+  static_assert(TT1 == 4 || TT1 == 8, "lane layout");
+  static_assert(TT1 == 8 || (5 * SB_RC) % 16 == 8, "phase-C bank groups");
 };
-constexpr int NB = 9;  // t1-pass outputs per (row, m, comp): V1 of 6 fields, D1 of Ql, Qr, C
-// shared-memory strides (in elements), padded so that half-warps hit 16 distinct 8-byte banks
-constexpr int SB_K = 2 * TT1;                // one slot k of sB: (m, a) = 16
-constexpr int SB_RC = NB * SB_K + 8;         // one (row, component) block of sB: 152
 
 template <typename T>
 constexpr size_t flux_smem_bytes() {
-  return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::TL2 * 5 * SB_RC);
+  return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::TL2 * 5 * FluxCfg<T>::SB_RC);
 }
 
 #ifndef HGKS_CP16
@@ -389,15 +404,18 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
 //      Ql, Qr, C on every row -> sB[l2][comp][slot][m][a]
 //   C  one thread per Gauss point: t2 pass, loaded lazily one derivative direction at a time,
 //      feeding the BGK flux (A4-A6); 4-point quadrature by warp shuffles (A7)
-// Lane layout in phase C: lane = 16 n + 8 m + a (a = t1 face in tile, (m, n) the Gauss point),
-// warp w = t2 face b, so every half-warp reads 16 consecutive (m, a) words of sB.
+// Lane layout in phase C: lane = 16 n + 2 TT1 bl + TT1 m + a (a = t1 face in tile, (m, n) the Gauss
+// point, t2 face b = BPW w + bl), so every half-warp reads 2 TT1 consecutive (m, a) words of sB from
+// each of its 16 / (2 TT1) rows, in disjoint bank groups.
 template <typename T, int DIR, int STAGE, bool PRF>
 __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl,
                 int fpb) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
-  constexpr int TT2 = FluxCfg<T>::TT2, TL2 = FluxCfg<T>::TL2, NTHREADS_FLUX = FluxCfg<T>::NT, SA_C = FluxCfg<T>::SA_C;
+  using Cfg = FluxCfg<T>;
+  constexpr int TT1 = Cfg::TT1, TL1 = Cfg::TL1, TL1P = Cfg::TL1P, TT2 = Cfg::TT2, TL2 = Cfg::TL2;
+  constexpr int NTHREADS_FLUX = Cfg::NT, SA_C = Cfg::SA_C, SB_K = Cfg::SB_K, SB_RC = Cfg::SB_RC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sA = reinterpret_cast<T*>(smem_raw);  // [6][5][SA_C]
   T* sB = sA + 6 * 5 * SA_C;               // [TL2][5][SB_RC]
@@ -419,12 +437,13 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     constexpr int VEC = 16 / (int)sizeof(T);  // lines per 16-byte chunk
     constexpr int NCH = TL1 / VEC;            // chunks per tile row
     // t1 is the contiguous axis of the array and every tile row of TL1 lines starts 16-byte aligned
-    // (ff_pitch, t10 % 8 == 0): 16-byte copies.  Tiles whose rows would run past line n1+1 (ragged
+    // (ff_pitch, t10 % 4 == 0): 16-byte copies.  Tiles whose rows would run past line n1+1 (ragged
     // edge) copy single lines, clamped.
     if (HGKS_CP16 && sizeof(T) == 8 && t10 + TL1 - 2 <= n1 + 2) {
       // item = (chunk, row l2, fc group): FS groups of 30/FS (field, component) planes each
       constexpr int NRC = TL2 * NCH;
-      constexpr int FS = (NTHREADS_FLUX / NRC) >= 6 ? 6 : ((NTHREADS_FLUX / NRC) >= 5 ? 5 : ((NTHREADS_FLUX / NRC) >= 3 ? 3 : 1));
+      constexpr int FSM = NTHREADS_FLUX / NRC;
+      constexpr int FS = FSM >= 6 ? 6 : (FSM >= 5 ? 5 : (FSM >= 3 ? 3 : (FSM >= 2 ? 2 : 1)));
       constexpr int FPG = 30 / FS;
       static_assert(30 % FS == 0, "fc groups");
       const int j = threadIdx.x;
@@ -432,7 +451,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
         const int ch = j % NCH, l2 = (j / NCH) % TL2, fg = j / NRC;
         const int t2 = min(t20 + l2 - 2, n2 + 1);
         const T* src = fbase + (long long)(fg * FPG) * fstride + L.line(t10 - 2 + ch * VEC, t2);
-        unsigned dst = sbase + (unsigned)(((fg * FPG) * SA_C + l2 * TL1 + ch * VEC) * (int)sizeof(T));
+        unsigned dst = sbase + (unsigned)(((fg * FPG) * SA_C + l2 * TL1P + ch * VEC) * (int)sizeof(T));
 #pragma unroll
         for (int f = 0; f < FPG; ++f) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -450,7 +469,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
           const int l1 = j % TL1, l2 = j / TL1;
           const int t1 = min(t10 + l1 - 2, n1 + 1), t2 = min(t20 + l2 - 2, n2 + 1);  // ragged tiles: clamp
           const T* src = fbase + L.line(t1, t2);
-          unsigned dst = sbase + (unsigned)((l2 * TL1 + l1) * sizeof(T));
+          unsigned dst = sbase + (unsigned)((l2 * TL1P + l1) * sizeof(T));
 #pragma unroll
           for (int fc = 0; fc < 30; ++fc) {
             if (sizeof(T) == 8)
@@ -489,17 +508,19 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   // ---- phase B: t1 pass on every row l2: value (6 fields) and t1-derivative (Ql, Qr, C) -----
   // One item = (a, c, l2) computes both Gauss abscissae m = 0, 1 from the same 30 loads: point
   // m = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
+  // Item order: TT1 = 8: (a, c, l2), a half-warp reads 2 components of one row; TT1 = 4: (a, l2, c),
+  // a half-warp reads 4 rows (TL1P apart) of one component -- both free of bank conflicts.
   for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
-    const int c = (w / TT1) % 5;
-    const int l2 = w / (TT1 * 5);
+    const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
+    const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
     T o0[NB], o1[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       o0[k] = T(0);
       o1[k] = T(0);
     }
-    const T* src = sA + c * SA_C + l2 * TL1 + a;
+    const T* src = sA + c * SA_C + l2 * TL1P + a;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
       const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
@@ -530,9 +551,10 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
 #endif
 
   // ---- phase C: one thread per Gauss point ----------------------------------------------------
+  // lane = 16 n + 2 TT1 bl + TT1 m + a; t2 face b = BPW warp + bl
   const int lane = threadIdx.x & 31;
-  const int a = lane & 7, m = (lane >> 3) & 1, nn = lane >> 4;
-  const int b = threadIdx.x >> 5;
+  const int a = lane % TT1, m = (lane / TT1) & 1, nn = lane >> 4;
+  const int b = (threadIdx.x >> 5) * Cfg::BPW + ((lane & 15) / (2 * TT1));
   const T ih1 = g.jg[A1][m * n1 + min(t10 + a, n1 - 1)], ih2 = g.jg[A2][nn * n2 + min(t20 + b, n2 - 1)];
   const T sgn = nn ? T(-1) : T(1);
   // t2 pass of slot k, component c, over rows b..b+4: value (wv) or derivative (wd) at this Gauss
@@ -628,18 +650,19 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     F[k] = gf.F[k];
     dF[k] = gf.dF[k];
   }
-  // 2x2 Gauss quadrature, omega_mn = 1/4 (O-8): the face's Gauss points sit at lanes a, a+8, a+16, a+24
+  // 2x2 Gauss quadrature, omega_mn = 1/4 (O-8): the face's Gauss points sit at lanes l, l ^ TT1 (m),
+  // l ^ 16 (n), l ^ TT1 ^ 16
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
     if (STAGE == 1) {
-      F[k] += __shfl_xor_sync(0xffffffffu, F[k], 8);
+      F[k] += __shfl_xor_sync(0xffffffffu, F[k], TT1);
       F[k] += __shfl_xor_sync(0xffffffffu, F[k], 16);
     }
-    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 8);
+    dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], TT1);
     dF[k] += __shfl_xor_sync(0xffffffffu, dF[k], 16);
   }
   const int f1 = t10 + a, f2 = t20 + b;
-  if (lane < 8 && f1 < n1 && f2 < n2) {
+  if (m == 0 && nn == 0 && f1 < n1 && f2 < n2) {
     int cd[3];
     cd[DIR] = fn;
     cd[A1] = f1;
