@@ -226,19 +226,28 @@ struct FluxCfg {
   // disjoint 4-bank groups); TT1 = 8 -> TL1 = 12
   static constexpr int TL1P = TL1 < 12 ? 12 : TL1;
   static constexpr int SA_C = TL2 * TL1P + 8;  // one (field, component) plane of sA
-  // sB: [TL2 rows][5 comps][SB_RC], slot k of a (row, comp) holds (m, a) = 2 TT1 words.  Pad so that
-  // the phase-C half-warps are conflict-free: TT1 = 8: 16 (m, a) words of one row; TT1 = 4: 8 words
-  // of each of two rows b, b+1, which are 5 SB_RC = 8 (mod 16) 8-byte words apart
+  // sB: the t1-pass outputs, word (row, comp c, slot k, m, a) at row RS + c CS + k KS + MA(m, a).
+  //   TT1 = 8: [row][c][k][m][a] (SB_RC = 152 words per (row, c), padded): a phase-C half-warp reads the
+  //            16 (m, a) words of one row; a phase-B warp stores (a, c) words of one row, c CS = 0, 24,
+  //            16, 8 (mod 32 4-byte banks) -- both conflict-free
+  //   TT1 = 4: [k][c][row][a][m]: a phase-C half-warp reads the 8 (a, m) words of two consecutive rows
+  //            b, b+1 = 16 consecutive words; a phase-B thread stores its (m = 0, m = 1) pair as one
+  //            16-byte word pair, a warp's 8 rows x 4 a = 64 consecutive words -- both conflict-free
   static constexpr int SB_K = 2 * TT1;
-  static constexpr int SB_RC = TT1 == 8 ? NB * SB_K + 8 : NB * SB_K;  // 152 / 72
+  static constexpr int SB_RC = NB * SB_K + 8;  // TT1 = 8 layout only
+  static constexpr int RS = TT1 == 8 ? 5 * SB_RC : 2 * TT1;
+  static constexpr int CS = TT1 == 8 ? SB_RC : TL2 * 2 * TT1;
+  static constexpr int KS = TT1 == 8 ? SB_K : 5 * TL2 * 2 * TT1;
+  static constexpr int SB_WORDS = TT1 == 8 ? TL2 * 5 * SB_RC : NB * KS;
+  __device__ static constexpr int MA(int m, int a) { return TT1 == 8 ? m * TT1 + a : 2 * a + m; }
   static constexpr int BPW = 16 / (2 * TT1);  // t2 faces per warp (lane = 16 n + 2 TT1 bl + TT1 m + a)
   static_assert(TT1 == 4 || TT1 == 8, "lane layout");
-  static_assert(TT1 == 8 || (5 * SB_RC) % 16 == 8, "phase-C bank groups");
+  static_assert(TT1 == 8 || sizeof(T) == 8, "the 4-wide tile's paired stores are 16-byte double2");
 };
 
 template <typename T>
 constexpr size_t flux_smem_bytes() {
-  return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::TL2 * 5 * FluxCfg<T>::SB_RC);
+  return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::SB_WORDS);
 }
 
 #ifndef HGKS_CP16
@@ -415,10 +424,10 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
   using Cfg = FluxCfg<T>;
   constexpr int TT1 = Cfg::TT1, TL1 = Cfg::TL1, TL1P = Cfg::TL1P, TT2 = Cfg::TT2, TL2 = Cfg::TL2;
-  constexpr int NTHREADS_FLUX = Cfg::NT, SA_C = Cfg::SA_C, SB_K = Cfg::SB_K, SB_RC = Cfg::SB_RC;
+  constexpr int NTHREADS_FLUX = Cfg::NT, SA_C = Cfg::SA_C, RS = Cfg::RS, CS = Cfg::CS, KS = Cfg::KS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sA = reinterpret_cast<T*>(smem_raw);  // [6][5][SA_C]
-  T* sB = sA + 6 * 5 * SA_C;               // [TL2][5][SB_RC]
+  T* sB = sA + 6 * 5 * SA_C;               // t1-pass outputs (FluxCfg: RS, CS, KS, MA)
 
   const int n1 = g.n[A1], n2 = g.n[A2];
   const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2;
@@ -535,11 +544,15 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
         if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
       }
     }
-    T* dst = sB + (l2 * 5 + c) * SB_RC + a;
+    T* dst = sB + l2 * RS + c * CS + Cfg::MA(0, a);
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-      dst[k * SB_K] = o0[k];
-      dst[k * SB_K + TT1] = o1[k];
+      if constexpr (TT1 == 4) {  // (m = 0, m = 1) adjacent: one 16-byte store
+        *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0[k], (double)o1[k]);
+      } else {
+        dst[k * KS] = o0[k];
+        dst[k * KS + Cfg::MA(1, 0)] = o1[k];
+      }
     }
   }
   if (do_ab) {
@@ -569,8 +582,8 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
 #define HGKS_ROW_MIRROR64 1
 #endif
   constexpr bool kRowMirror = sizeof(T) == 8 && HGKS_ROW_MIRROR64;
-  const T* row0 = sB + m * TT1 + a + (b + (kRowMirror && nn ? 4 : 0)) * (5 * SB_RC);
-  const int rstep = (kRowMirror && nn) ? -5 * SB_RC : 5 * SB_RC;
+  const T* row0 = sB + Cfg::MA(m, a) + (b + (kRowMirror && nn ? 4 : 0)) * RS;
+  const int rstep = (kRowMirror && nn) ? -RS : RS;
   T wvl[5], wdl[5];
 #pragma unroll
   for (int r = 0; r < 5; ++r) {
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   auto tv = [&](int c, int k) {
     if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
     if (HGKS_TV_SPLIT) {
-      const T* p = row0 + c * SB_RC + k * SB_K;
+      const T* p = row0 + c * CS + k * KS;
       const T a0 = (kRowMirror ? wv0<T>(0) : wvl[0]) * p[0] + (kRowMirror ? wv0<T>(2) : wvl[2]) * p[2 * rstep] +
                    (kRowMirror ? wv0<T>(4) : wvl[4]) * p[4 * rstep];
       const T a1 = (kRowMirror ? wv0<T>(1) : wvl[1]) * p[rstep] + (kRowMirror ? wv0<T>(3) : wvl[3]) * p[3 * rstep];
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     }
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wv0<T>(r) : wvl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wv0<T>(r) : wvl[r]) * row0[r * rstep + c * CS + k * KS];
     return v;
   };
   // row mirror: the derivative of a mirrored row stream carries the sign sgn, folded into ih2s (every
@@ -604,7 +617,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
     T v = T(0);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wd0<T>(r) : wdl[r]) * row0[r * rstep + c * SB_RC + k * SB_K];
+    for (int r = 0; r < 5; ++r) v += (kRowMirror ? wd0<T>(r) : wdl[r]) * row0[r * rstep + c * CS + k * KS];
     return v;
   };
   const T dt = T(ctl->dt);
@@ -617,7 +630,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     d = T(0);
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
-      const T x = row0[r * rstep + c * SB_RC + k * SB_K];
+      const T x = row0[r * rstep + c * CS + k * KS];
       v += (kRowMirror ? wv0<T>(r) : wvl[r]) * x;
       d += (kRowMirror ? wd0<T>(r) : wdl[r]) * x;
     }
