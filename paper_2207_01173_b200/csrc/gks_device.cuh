@@ -547,11 +547,11 @@ struct GpFlux {
 #ifndef HGKS_HFAST
 #define HGKS_HFAST 1
 #endif
-    // fp32 only: in fp64 the tables and the merged slope raise register pressure (more spills) and
-    // measured 0.6 % slower despite 30 fewer FP64 instructions per Gauss point (fp32: +0.9 %).  The
-    // Pr-fix variant keeps the generic H (its heat-flux density terms reuse e, f).
+    // fp32 +0.9 %; fp64: 45 fewer FP64 instructions per Gauss point, +1.5 % at 256^3 with the 4 x 8
+    // tile (round 1, at 2 blocks per SM with spills, it measured 0.6 % slower).  The Pr-fix variant
+    // keeps the generic H (its heat-flux density terms reuse e, f).
 #ifndef HGKS_HFAST64
-#define HGKS_HFAST64 0
+#define HGKS_HFAST64 1
 #endif
     constexpr bool kHfast = HGKS_HFAST && !PRF && (sizeof(T) == 4 || HGKS_HFAST64);
     // moment tables of this side: sn[n] = (t_{n+2} + k2 t_n)/2, tth[n] = theta t_n, so that

@@ -201,6 +201,9 @@ __device__ __forceinline__ void block_sum_warps(double (&v)[N], double* sh) {
 #ifndef HGKS_TT1_64
 #define HGKS_TT1_64 4
 #endif
+#ifndef HGKS_VEC32
+#define HGKS_VEC32 0  // fp32: vectorised sB layout (FluxCfg::VEC)
+#endif
 #ifndef HGKS_TT2_64
 #define HGKS_TT2_64 8
 #endif
@@ -223,8 +226,9 @@ struct FluxCfg {
   static constexpr int NT = TT1 * TT2 * 4;                                    // threads: one per Gauss point
   static constexpr int MINB = sizeof(T) == 8 ? HGKS_FLUX_MINB : HGKS_FLUX_MINB32;
   // sA row pitch: TT1 = 4 -> 12 (phase-B half-warps read 4 rows of 4 lines: rows 12 apart hit 4
-  // disjoint 4-bank groups); TT1 = 8 -> TL1 = 12
-  static constexpr int TL1P = TL1 < 12 ? 12 : TL1;
+  // disjoint 4-slot groups of a 16-slot wavefront); TT1 = 8 -> TL1 = 12.  (fp32 with items (a, l2, c)
+  // and a conflict-free pitch of 24 measured 6 % slower: 35 KB instead of 18 KB of sA per block.)
+  static constexpr int TL1P = 12;
   static constexpr int SA_C = TL2 * TL1P + 8;  // one (field, component) plane of sA
   // sB: the t1-pass outputs, word (row, comp c, slot k, m, a) at row RS + c CS + k KS + MA(m, a).
   //   TT1 = 8: [row][c][k][m][a] (SB_RC = 152 words per (row, c), padded): a phase-C half-warp reads the
@@ -233,12 +237,19 @@ struct FluxCfg {
   //   TT1 = 4: [k][c][row][a][m]: a phase-C half-warp reads the 8 (a, m) words of two consecutive rows
   //            b, b+1 = 16 consecutive words; a phase-B thread stores its (m = 0, m = 1) pair as one
   //            16-byte word pair, a warp's 8 rows x 4 a = 64 consecutive words -- both conflict-free
+  //   VEC (fp32, HGKS_VEC32): [row][k][comps 0-3 of the 16 (m, a) as float4 | comp 4 of the 16 (m, a)],
+  //            so phase C reads the five components of one (row, slot) with one 16-byte and one 4-byte
+  //            load (2 instead of 5 issue slots; fp32 is issue-bound)
+  static constexpr bool VEC = sizeof(T) == 4 && HGKS_VEC32;
   static constexpr int SB_K = 2 * TT1;
   static constexpr int SB_RC = NB * SB_K + 8;  // TT1 = 8 layout only
-  static constexpr int RS = TT1 == 8 ? 5 * SB_RC : 2 * TT1;
+  static constexpr int VK = 5 * 2 * TT1;       // VEC: words per (row, k)
+  static constexpr int RS = VEC ? NB * VK : (TT1 == 8 ? 5 * SB_RC : 2 * TT1);
   static constexpr int CS = TT1 == 8 ? SB_RC : TL2 * 2 * TT1;
-  static constexpr int KS = TT1 == 8 ? SB_K : 5 * TL2 * 2 * TT1;
-  static constexpr int SB_WORDS = TT1 == 8 ? TL2 * 5 * SB_RC : NB * KS;
+  static constexpr int KS = VEC ? VK : (TT1 == 8 ? SB_K : 5 * TL2 * 2 * TT1);
+  static constexpr int SB_WORDS = VEC ? TL2 * RS : (TT1 == 8 ? TL2 * 5 * SB_RC : NB * KS);
+  // VEC: offset of component c of (m, a) within a (row, k) block
+  __device__ static constexpr int VOFF(int c, int ma) { return c < 4 ? 4 * ma + c : 8 * TT1 + ma; }
   __device__ static constexpr int MA(int m, int a) { return TT1 == 8 ? m * TT1 + a : 2 * a + m; }
   static constexpr int BPW = 16 / (2 * TT1);  // t2 faces per warp (lane = 16 n + 2 TT1 bl + TT1 m + a)
   static_assert(TT1 == 4 || TT1 == 8, "lane layout");
@@ -518,7 +529,8 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   // One item = (a, c, l2) computes both Gauss abscissae m = 0, 1 from the same 30 loads: point
   // m = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r].
   // Item order: TT1 = 8: (a, c, l2), a half-warp reads 2 components of one row; TT1 = 4: (a, l2, c),
-  // a half-warp reads 4 rows (TL1P apart) of one component -- both free of bank conflicts.
+  // a half-warp reads 4 rows (TL1P apart) of one component -- conflict-free (TT1 = 8 except where a
+  // warp straddles two rows).
   for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
     const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
@@ -544,10 +556,13 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
         if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
       }
     }
-    T* dst = sB + l2 * RS + c * CS + Cfg::MA(0, a);
+    T* dst = sB + l2 * RS + (Cfg::VEC ? 0 : c * CS + Cfg::MA(0, a));
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-      if constexpr (TT1 == 4) {  // (m = 0, m = 1) adjacent: one 16-byte store
+      if constexpr (Cfg::VEC) {
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(0, a))] = o0[k];
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(1, a))] = o1[k];
+      } else if constexpr (TT1 == 4) {  // (m = 0, m = 1) adjacent: one 16-byte store
         *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0[k], (double)o1[k]);
       } else {
         dst[k * KS] = o0[k];
@@ -636,6 +651,59 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     }
   };
   T d2l[5], d2r[5];
+  if constexpr (Cfg::VEC) {
+    // five components of slot k per row: one float4 + one float load (VOFF layout); weights w[r]
+    const T* rv = sB + b * RS + 4 * Cfg::MA(m, a);
+    const T* rs = sB + b * RS + 8 * TT1 + Cfg::MA(m, a);
+    auto pass5 = [&](int k, const T (&w)[5], T (&o)[5]) {
+      if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        const float4 x = *reinterpret_cast<const float4*>(rv + r * rstep + k * KS);
+        const T x4 = rs[r * rstep + k * KS];
+        o[0] = r ? o[0] + w[r] * x.x : w[r] * x.x;
+        o[1] = r ? o[1] + w[r] * x.y : w[r] * x.y;
+        o[2] = r ? o[2] + w[r] * x.z : w[r] * x.z;
+        o[3] = r ? o[3] + w[r] * x.w : w[r] * x.w;
+        o[4] = r ? o[4] + w[r] * x4 : w[r] * x4;
+      }
+    };
+    auto pass5vd = [&](int k, T (&v)[5], T (&d)[5]) {
+      if (HGKS_TV_FENCE) asm volatile("" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        const float4 x = *reinterpret_cast<const float4*>(rv + r * rstep + k * KS);
+        const T x4 = rs[r * rstep + k * KS];
+        const T xs[5] = {x.x, x.y, x.z, x.w, x4};
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          v[c] = r ? v[c] + wvl[r] * xs[c] : wvl[r] * xs[c];
+          d[c] = r ? d[c] + wdl[r] * xs[c] : wdl[r] * xs[c];
+        }
+      }
+    };
+    {
+      T Wl[5], Wr[5];
+      pass5vd(0, Wl, d2l);
+      pass5vd(1, Wr, d2r);
+      gf.begin(gas, Wl, Wr, dt, T(1) / dt);
+    }
+    gf.template add_side<+1>([&](int i, T (&d)[5]) {
+      if (i == 0) pass5(2, wvl, d);
+      if (i == 1) { pass5(6, wvl, d); for (int c = 0; c < 5; ++c) d[c] *= ih1; }
+      if (i == 2) for (int c = 0; c < 5; ++c) d[c] = d2l[c] * ih2s;
+    });
+    gf.template add_side<-1>([&](int i, T (&d)[5]) {
+      if (i == 0) pass5(3, wvl, d);
+      if (i == 1) { pass5(7, wvl, d); for (int c = 0; c < 5; ++c) d[c] *= ih1; }
+      if (i == 2) for (int c = 0; c < 5; ++c) d[c] = d2r[c] * ih2s;
+    });
+    gf.add_equilibrium([&](int i, T (&d)[5]) {
+      if (i == 0) pass5(5, wvl, d);
+      if (i == 1) { pass5(8, wvl, d); for (int c = 0; c < 5; ++c) d[c] *= ih1; }
+      if (i == 2) { pass5(4, wdl, d); for (int c = 0; c < 5; ++c) d[c] *= ih2s; }
+    });
+  } else {
   {
     T Wl[5], Wr[5];
 #pragma unroll
@@ -657,6 +725,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
 #pragma unroll
     for (int c = 0; c < 5; ++c) d[c] = i == 0 ? tv(c, 5) : (i == 1 ? tv(c, 8) * ih1 : td(c, 4) * ih2s);
   });
+  }
   T F[5], dF[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
