@@ -863,11 +863,20 @@ __device__ __forceinline__ double wave_speed(const T (&c5)[5], const Geo<T>& g, 
   return fmax(sx, fmax(sy, sz));
 }
 
+// Block max of s, then ONE atomicMax per block on the bit pattern (which orders non-negative doubles).
+// Every thread of the block must call it.  (One atomic per warp -- 524k atomics on one address per
+// stage-2 update at 256^3 -- serialised in the L2 atomic unit.)
 __device__ __forceinline__ void block_max_commit(double s, unsigned long long* dst) {
-  // warp max, then one atomic per warp (atomicMax on the bit pattern orders non-negative doubles)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0 && s > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(s));
+  __shared__ double wmax[32];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int w = 1; w < nw; ++w) s = fmax(s, wmax[w]);
+    if (s > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(s));
+  }
 }
 
 // ---- flux divergence + S2O4 stage update (Eqs. (3)-(4), (7)) ----------------------------------
