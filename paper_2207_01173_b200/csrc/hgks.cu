@@ -689,9 +689,11 @@ static int run_steps(hgks_ctx* c, int nsteps) {
     if ((rc = flux_sweeps<T, 1>(c, Qn))) return rc;
     prof_begin(c, HGKS_K_UPDATE);
     if (c->hist_cap > 0) {  // + volume diagnostics of Q^n (per-step history, NEXT-2)
-      update_kernel<T, 1, true><<<ugrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg,
+      const dim3 dgrid((g.n[0] + UPDD_X - 1) / UPDD_X, (g.n[1] + UPDD_Y - 1) / UPDD_Y, g.n[2]);
+      update_kernel<T, 1, true><<<dgrid, tpb, 0, c->s>>>(Qn, Qs, R, (T*)c->F[0], (T*)c->F[1], (T*)c->F[2], g, dg,
                                                            c->p.gamma, c->ctl, c->bulk_dev, c->dpart);
-      hist_reduce_kernel<<<HIST_RB, DIAG_TPB, 0, c->s>>>(c->dpart, ublocks, c->dpart2, c->ctl);
+      hist_reduce_kernel<<<HIST_RB, DIAG_TPB, 0, c->s>>>(c->dpart, (long long)dgrid.x * dgrid.y * dgrid.z, c->dpart2,
+                                                         c->ctl);
       hist_final_kernel<<<1, DIAG_TPB, 0, c->s>>>(c->dpart2, c->hist, c->hist_td, c->ctl);
       c->total_launches += 2;
     } else {
@@ -1174,7 +1176,7 @@ int hgks_history_enable(hgks_ctx* c, int32_t capacity, double rho0) {
   c->hist_pending = 0;
   c->hist_rho0 = rho0;
   if (capacity > 0) {
-    const size_t ublocks = (size_t)((c->n[0] + UPD_X - 1) / UPD_X) * ((c->n[1] + UPD_Y - 1) / UPD_Y) * c->nzl;
+    const size_t ublocks = (size_t)((c->n[0] + UPDD_X - 1) / UPDD_X) * ((c->n[1] + UPDD_Y - 1) / UPDD_Y) * c->nzl;
     bool ok = cudaMalloc(&c->dpart, ublocks * NDIAG * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->dpart2, (size_t)HIST_RB * NDIAG * sizeof(double)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->hist, (size_t)capacity * NDIAG * sizeof(double)) == cudaSuccess;
@@ -1394,6 +1396,7 @@ static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
   CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
   SYNC_TRY(c);
   h->dt = dt;
+  h->idt = 1.0 / dt;
   h->halt = 0;
   CUDA_TRY(c, cudaMemcpyAsync(c->ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, c->s));
   int rc;

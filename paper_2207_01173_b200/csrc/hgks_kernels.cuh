@@ -45,6 +45,7 @@ struct Ctl {
   double m_prev, dt_prev, f_prev;  // controller memory: previous step's m, dt and f
   double bulk_new[2];           // (sum rho dV, sum rho U dV) of the newest state (allreduced)
   int hist_n, hist_cap;         // per-step diagnostic history: rows written / capacity
+  double idt;                   // 1 / dt of the step in flight (one IEEE division per step, not per Gauss point)
 };
 
 template <typename T>
@@ -263,6 +264,9 @@ constexpr size_t flux_smem_bytes() {
   return sizeof(T) * (6 * 5 * FluxCfg<T>::SA_C + FluxCfg<T>::SB_WORDS);
 }
 
+#ifndef HGKS_CP16_32
+#define HGKS_CP16_32 0  // 16-byte face-field copies for fp32 (4 lines per chunk): measured neutral
+#endif
 #ifndef HGKS_CP16
 #define HGKS_CP16 1  // 16-byte face-field copies (fp64): +7 % fp64 step rate (x, z sweeps); no gain fp32
 #endif
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     // t1 is the contiguous axis of the array and every tile row of TL1 lines starts 16-byte aligned
     // (ff_pitch, t10 % 4 == 0): 16-byte copies.  Tiles whose rows would run past line n1+1 (ragged
     // edge) copy single lines, clamped.
-    if (HGKS_CP16 && sizeof(T) == 8 && t10 + TL1 - 2 <= n1 + 2) {
+    if ((sizeof(T) == 8 ? HGKS_CP16 : HGKS_CP16_32) && t10 + TL1 - 2 <= n1 + 2) {
       // item = (chunk, row l2, fc group): FS groups of 30/FS (field, component) planes each
       constexpr int NRC = TL2 * NCH;
       constexpr int FSM = NTHREADS_FLUX / NRC;
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
       T Wl[5], Wr[5];
       pass5vd(0, Wl, d2l);
       pass5vd(1, Wr, d2r);
-      gf.begin(gas, Wl, Wr, dt, T(1) / dt);
+      gf.begin(gas, Wl, Wr, dt, T(ctl->idt));
     }
     gf.template add_side<+1>([&](int i, T (&d)[5]) {
       if (i == 0) pass5(2, wvl, d);
@@ -715,7 +719,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
       tvd(c, 0, Wl[c], d2l[c]);
       tvd(c, 1, Wr[c], d2r[c]);
     }
-    gf.begin(gas, Wl, Wr, dt, T(1) / dt);
+    gf.begin(gas, Wl, Wr, dt, T(ctl->idt));
   }
   gf.template add_side<+1>([&](int i, T (&d)[5]) {
 #pragma unroll
@@ -893,6 +897,12 @@ __device__ __forceinline__ void block_max_commit(double s, unsigned long long* d
 // the gradients of Q^{n+1} (its neighbours are written by other blocks of the same launch), so the
 // history holds the state at the START of every step; the final state is one hgks_diagnostics call.
 constexpr int UPD_X = 64, UPD_Y = DIAG_TPB / UPD_X;  // update_kernel block shape (DIAG_TPB threads)
+// stage-1 update with the per-step history: 32 x 8 cells, so the staged velocity tile (+-2 halo) is
+// 36 x 12 = 432 cells per 256 instead of 68 x 8 = 544
+#ifndef HGKS_UPDD_X
+#define HGKS_UPDD_X 32
+#endif
+constexpr int UPDD_X = HGKS_UPDD_X, UPDD_Y = DIAG_TPB / UPDD_X;
 template <typename T, int STAGE, bool DIAG = false>
 __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
@@ -901,8 +911,9 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
   if (ctl->halt) return;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   // block = UPD_X x UPD_Y cells of one z plane (grid: x tiles, y tiles, z): no index divisions
-  const int i = blockIdx.x * UPD_X + (threadIdx.x % UPD_X);
-  const int j = blockIdx.y * UPD_Y + (threadIdx.x / UPD_X);
+  constexpr int UX = DIAG ? UPDD_X : UPD_X, UY = DIAG ? UPDD_Y : UPD_Y;
+  const int i = blockIdx.x * UX + (threadIdx.x % UX);
+  const int j = blockIdx.y * UY + (threadIdx.x / UX);
   const int k = blockIdx.z;
   const double dt = ctl->dt;
   const int fmode = ctl->force_mode;
@@ -981,11 +992,11 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
     for (int n = 0; n < NDIAG; ++n) acc[n] = 0.0;
     // velocities of the block's 64 x 4 cells and their +-2 x/y halo, one reciprocal each, staged in
     // shared memory; the z neighbours (other planes) come from global memory
-    constexpr int TX = UPD_X + 4, TY = UPD_Y + 4;
+    constexpr int TX = UX + 4, TY = UY + 4;
     __shared__ double su[3][TY][TX];
     for (int e = threadIdx.x; e < TX * TY; e += DIAG_TPB) {
       const int lx = e % TX, ly = e / TX;
-      const int gi = blockIdx.x * UPD_X + lx - 2, gj = blockIdx.y * UPD_Y + ly - 2;
+      const int gi = blockIdx.x * UX + lx - 2, gj = blockIdx.y * UY + ly - 2;
       if (gi <= nx + 2 && gj <= ny + 2) {
         double uu[3];
         vel_of(Q, g, gi, gj, k, uu);
@@ -995,7 +1006,7 @@ __global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ 
     }
     __syncthreads();
     if (i < nx && j < ny) {
-      const int lx = threadIdx.x % UPD_X + 2, ly = threadIdx.x / UPD_X + 2;
+      const int lx = threadIdx.x % UX + 2, ly = threadIdx.x / UX + 2;
       const double vol = dg.w[0][i] * dg.w[1][j] * dg.w[2][k];
       const double rho = (double)Q[qidx(g, 0, i, j, k)];
       double u[3], m[3];
@@ -1151,6 +1162,7 @@ __global__ void dt_kernel(Ctl* c) {
     if (dt > rem) dt = rem;
   }
   c->dt = dt;
+  c->idt = 1.0 / dt;
   if (c->force_mode == 1) {
     c->force = c->f_init;
   } else if (c->force_mode == 2) {  // O-27
