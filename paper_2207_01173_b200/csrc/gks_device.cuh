@@ -77,6 +77,50 @@ __host__ __device__ __forceinline__ double half_erfc(double x) {
   }
   return 0.5 * erfc(x);
 }
+// erfc(x)/2 and exp(-x^2) together (the two transcendental factors of the half-space moments t0, t1 of one
+// side, A.2).  |x| < 0.75: the erf series above and the Taylor series of e^{-z}, z = x^2 (18 terms,
+// truncation < 3e-19 relative at z = 0.5625), each as two Horner chains in w = z^2, so four independent
+// dependency chains of depth <= 9 replace the 13-deep erf chain plus libdevice exp; else erfc and exp.
+#ifndef HGKS_SERIES_EXP
+#define HGKS_SERIES_EXP 2
+#endif
+#ifndef HGKS_LATE_GAMMA
+#define HGKS_LATE_GAMMA 1
+#endif
+#define HGKS_INVFACT 1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333, 0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11, 7.647163731819816e-13, 4.779477332387385e-14, 2.8114572543455206e-15
+#ifdef __CUDACC__
+__constant__ double c_invfact[18] = {HGKS_INVFACT};
+#endif
+__host__ __device__ __forceinline__ double invfact(int n) {
+#ifdef __CUDA_ARCH__
+  return c_invfact[n];
+#else
+  constexpr double k[18] = {HGKS_INVFACT};
+  return k[n];
+#endif
+}
+__host__ __device__ __forceinline__ void half_erfc_exp(double x, double& he, double& ex) {
+  if (fabs(x) < 0.75) {
+    const double z = x * x, w = z * z;
+    double a = erfc_series_coef(1), b = erfc_series_coef(0);
+    double e = invfact(16), o = invfact(17);  // e^{-z} = E(w) - z O(w), E = sum w^j/(2j)!, O = sum w^j/(2j+1)!
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {
+      a = fma(a, w, erfc_series_coef(2 * i + 1));
+      b = fma(b, w, erfc_series_coef(2 * i));
+    }
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+      e = fma(e, w, invfact(2 * j));
+      o = fma(o, w, invfact(2 * j + 1));
+    }
+    he = fma(-0.56418958354775628694807945156077 * x, fma(b, z, a), 0.5);
+    ex = fma(-z, o, e);
+    return;
+  }
+  he = 0.5 * erfc(x);
+  ex = exp(-x * x);
+}
 #ifndef HGKS_FAST_ERFC32
 #define HGKS_FAST_ERFC32 1
 #endif
@@ -94,6 +138,41 @@ __host__ __device__ __forceinline__ float half_erfc(float x) {
   return 0.5f * erfcf(x);
 }
 __host__ __device__ __forceinline__ float m_erfc(float x) { return erfcf(x); }
+// both sides at once, one branch: with both |x| < 0.75 the eight Horner chains share one basic block, so
+// the scheduler interleaves the left and right series (two separate calls leave a branch between them)
+__host__ __device__ __forceinline__ void half_erfc_exp2(double xl, double xr, double& hel, double& exl, double& her,
+                                                        double& exr) {
+  if (fabs(xl) < 0.75 && fabs(xr) < 0.75) {
+    const double zl = xl * xl, wl = zl * zl, zr = xr * xr, wr = zr * zr;
+    double al = erfc_series_coef(1), bl = erfc_series_coef(0), ar = al, br = bl;
+    double el = invfact(16), ol = invfact(17), er = el, orr = ol;
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {
+      al = fma(al, wl, erfc_series_coef(2 * i + 1));
+      bl = fma(bl, wl, erfc_series_coef(2 * i));
+      ar = fma(ar, wr, erfc_series_coef(2 * i + 1));
+      br = fma(br, wr, erfc_series_coef(2 * i));
+    }
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+      el = fma(el, wl, invfact(2 * j));
+      ol = fma(ol, wl, invfact(2 * j + 1));
+      er = fma(er, wr, invfact(2 * j));
+      orr = fma(orr, wr, invfact(2 * j + 1));
+    }
+    hel = fma(-0.56418958354775628694807945156077 * xl, fma(bl, zl, al), 0.5);
+    exl = fma(-zl, ol, el);
+    her = fma(-0.56418958354775628694807945156077 * xr, fma(br, zr, ar), 0.5);
+    exr = fma(-zr, orr, er);
+    return;
+  }
+  half_erfc_exp(xl, hel, exl);
+  half_erfc_exp(xr, her, exr);
+}
+__host__ __device__ __forceinline__ void half_erfc_exp(float x, float& he, float& ex) {
+  he = half_erfc(x);
+  ex = expf(-x * x);
+}
 __host__ __device__ __forceinline__ double m_pow(double x, double y) { return pow(x, y); }
 __host__ __device__ __forceinline__ float m_pow(float x, float y) { return powf(x, y); }
 __host__ __device__ __forceinline__ double m_abs(double x) { return fabs(x); }
@@ -353,10 +432,22 @@ struct GpFlux {
     thr = T(0.5) * k3 * (WR[4] * irr - T(0.5) * (Ur * Ur + Vr * Vr + Wr * Wr));
     // half-space seeds (A.2): sqrt(lambda) = rsqrt(2 theta), 1/sqrt(lambda) = 2 theta rsqrt(2 theta)
     const T sl = m_rsqrt(T(2) * thl), sr = m_rsqrt(T(2) * thr);
-    hl0 = half_erfc(-sl * Ul);
-    hl1 = Ul * hl0 + isqpi * thl * sl * m_exp(-sl * sl * Ul * Ul);
-    hr0 = half_erfc(sr * Ur);
-    hr1 = Ur * hr0 - isqpi * thr * sr * m_exp(-sr * sr * Ur * Ur);
+    if constexpr (HGKS_SERIES_EXP && sizeof(T) == 8) {
+      T el, er;
+      if (HGKS_SERIES_EXP == 2) {
+        half_erfc_exp2(-sl * Ul, sr * Ur, hl0, el, hr0, er);
+      } else {
+        half_erfc_exp(-sl * Ul, hl0, el);
+        half_erfc_exp(sr * Ur, hr0, er);
+      }
+      hl1 = Ul * hl0 + isqpi * thl * sl * el;
+      hr1 = Ur * hr0 - isqpi * thr * sr * er;
+    } else {
+      hl0 = half_erfc(-sl * Ul);
+      hl1 = Ul * hl0 + isqpi * thl * sl * m_exp(-sl * sl * Ul * Ul);
+      hr0 = half_erfc(sr * Ur);
+      hr1 = Ur * hr0 - isqpi * thr * sr * m_exp(-sr * sr * Ur * Ur);
+    }
     // Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
     const T hl2 = Ul * hl1 + thl * hl0, hr2 = Ur * hr1 + thr * hr0;
     const T q0 = rl * hl0 + rr * hr0;
@@ -374,6 +465,19 @@ struct GpFlux {
     // tau = mu(T0)/p0 with T0 = theta0, p0 = rho0 theta0 (O-9)
     const T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
     tau = qdiv(mu * ir0, th0);
+    if (!HGKS_LATE_GAMMA) finish_gamma();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      F[k] = T(0);
+      dF[k] = T(0);
+    }
+  }
+
+  // h and the shared Gamma / Gamma' factors.  HGKS_LATE_GAMMA: called by add_side<+1> just before its
+  // first use, so that the warp-uniform branch of the h exponential does not separate the tau chain of
+  // begin() from the slope work of the first side (independent of tau) -- the scheduler can interleave
+  // them within one basic block
+  HD void finish_gamma() {
     // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
     // (below 1e-20 -- dt/tau > 92, e.g. every low-Mach TGV face -- h changes no Gamma above rounding)
     const T harg = -T(0.5) * dt * rcp(tau);
@@ -396,11 +500,6 @@ struct GpFlux {
       gp1 = T(4) * tau * om * om * idt2;
       gp2 = T(4) * tau * om * (dt * h - T(2) * tau * om) * idt2;
       tgp1 = tau * gp1;
-    }
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      F[k] = T(0);
-      dF[k] = T(0);
     }
   }
 
@@ -644,6 +743,7 @@ struct GpFlux {
     if (kHfast) Hf(A, 1, Y);
     else H(A, 1, T(1), Y);
     T Z[5] = {t[1], t[2], T(0), T(0), sn[1]};
+    if (HGKS_LATE_GAMMA && SIDE > 0) finish_gamma();
     if (PRF) {
       // heat flux relative to U0 (O-12) from the flux vectors (Z, X, Y) and the density vectors
       // (Zd, Xd, Yd) = <psi>, sum_i <u_i a_i.psi psi>, <A.psi psi> of this side, all in its
