@@ -23,9 +23,27 @@ namespace hgks {
 // ---------------------------------------------------------------------------------------------
 // precision-generic math
 // ---------------------------------------------------------------------------------------------
+#ifndef HGKS_RSQRT_NR
+#define HGKS_RSQRT_NR 1
+#endif
 __host__ __device__ __forceinline__ double m_sqrt(double x) { return sqrt(x); }
 __host__ __device__ __forceinline__ float m_sqrt(float x) { return sqrtf(x); }
-__host__ __device__ __forceinline__ double m_rsqrt(double x) { return rsqrt(x); }
+// 1/sqrt(x) for the normal positive operands of the scheme (2 theta): MUFU seed + two Newton steps, no
+// slow-path branch (libdevice rsqrt branches to a special-case path, splitting the Gauss-point code into
+// basic blocks the scheduler cannot interleave across).  Host builds use the library.
+__host__ __device__ __forceinline__ double m_rsqrt(double x) {
+#ifdef __CUDA_ARCH__
+  if (HGKS_RSQRT_NR) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+    y = fma(0.5 * y, e, y);
+    e = fma(-x * y, y, 1.0);
+    return fma(0.5 * y, e, y);
+  }
+#endif
+  return rsqrt(x);
+}
 __host__ __device__ __forceinline__ float m_rsqrt(float x) { return rsqrtf(x); }
 __host__ __device__ __forceinline__ double m_exp(double x) { return exp(x); }
 __host__ __device__ __forceinline__ float m_exp(float x) { return expf(x); }
@@ -393,7 +411,9 @@ HD void temporal_slope(T K, T ik3, T th, T it, const T (&R)[5], T (&A)[5]) {
 //   add_side<+1>(load_l), add_side<-1>(load_r)   g_l H(u) and g_r (1 - H(u)) terms (Gamma_4..6)
 //   add_equilibrium(load_0)        g0 terms of Eq. (6) (Gamma_1..3)
 // Results: F (if NEED_F), dF, tau.  Invalid input propagates as NaN.
-template <typename T, bool NEED_F, bool PRF = false>
+// MU: viscosity law known at compile time (0 constant, 1 power law) or -1 (GasK::mu_law at run time); a
+// compile-time law keeps the uniform branch around pow() out of the Gauss-point code
+template <typename T, bool NEED_F, bool PRF = false, int MU = -1>
 struct GpFlux {
   T K;
   T rl, irl, Ul, Vl, Wl, thl, hl0, hl1;
@@ -463,7 +483,14 @@ struct GpFlux {
     W0 = q3 * ir0;
     th0 = T(0.5) * k3 * (q4 * ir0 - T(0.5) * (U0 * U0 + V0 * V0 + W0 * W0));
     // tau = mu(T0)/p0 with T0 = theta0, p0 = rho0 theta0 (O-9)
-    const T mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
+    T mu;
+    if constexpr (MU == 0) {
+      mu = g.mu_ref;
+    } else if constexpr (MU == 1) {
+      mu = g.mu_ref * m_pow(th0 / g.T_ref, g.omega);
+    } else {
+      mu = (g.mu_law == 1) ? g.mu_ref * m_pow(th0 / g.T_ref, g.omega) : g.mu_ref;
+    }
     tau = qdiv(mu * ir0, th0);
     if (!HGKS_LATE_GAMMA) finish_gamma();
 #pragma unroll

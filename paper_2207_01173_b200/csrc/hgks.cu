@@ -494,12 +494,19 @@ template <typename T, int STAGE>
 static int set_flux_attrs(hgks_ctx* c) {
   if (c->flux_attr_set[STAGE - 1]) return HGKS_OK;
   const int sm = (int)flux_smem_bytes<T>();
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 0, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 1, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  CUDA_TRY(c, cudaFuncSetAttribute(flux_kernel<T, 2, STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  auto set = [&](auto kern) -> cudaError_t { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); };
+  CUDA_TRY(c, set(flux_kernel<T, 0, STAGE, 0>));
+  CUDA_TRY(c, set(flux_kernel<T, 1, STAGE, 0>));
+  CUDA_TRY(c, set(flux_kernel<T, 2, STAGE, 0>));
+  CUDA_TRY(c, set(flux_kernel<T, 0, STAGE, 1>));
+  CUDA_TRY(c, set(flux_kernel<T, 1, STAGE, 1>));
+  CUDA_TRY(c, set(flux_kernel<T, 2, STAGE, 1>));
+  CUDA_TRY(c, set(flux_kernel<T, 0, STAGE, 2>));
+  CUDA_TRY(c, set(flux_kernel<T, 1, STAGE, 2>));
+  CUDA_TRY(c, set(flux_kernel<T, 2, STAGE, 2>));
+  CUDA_TRY(c, set(flux_kernel<T, 0, STAGE, 3>));
+  CUDA_TRY(c, set(flux_kernel<T, 1, STAGE, 3>));
+  CUDA_TRY(c, set(flux_kernel<T, 2, STAGE, 3>));
   c->flux_attr_set[STAGE - 1] = true;
   return HGKS_OK;
 }
@@ -614,13 +621,24 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
     dim3 grid((n1 + TT1 - 1) / TT1, (n2 + TT2 - 1) / TT2, (n3[d] + 1 + fpb - 1) / fpb);
     CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_rec[d], 0));
     prof_begin(c, HGKS_K_FLUX_X + d);
-    const bool prf = c->p.prandtl != 1.0;
-    if (d == 0 && !prf) flux_kernel<T, 0, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
-    if (d == 1 && !prf) flux_kernel<T, 1, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
-    if (d == 2 && !prf) flux_kernel<T, 2, STAGE, false><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
-    if (d == 0 && prf) flux_kernel<T, 0, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[0], g, gas, c->ctl, fpb);
-    if (d == 1 && prf) flux_kernel<T, 1, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[1], g, gas, c->ctl, fpb);
-    if (d == 2 && prf) flux_kernel<T, 2, STAGE, true><<<grid, FluxCfg<T>::NT, smem, c->s>>>(ff, (T*)c->F[2], g, gas, c->ctl, fpb);
+    // flux_kernel VAR: bit 0 = Pr != 1 (heat-flux fix), bit 1 = power-law viscosity
+    const int var = (c->p.prandtl != 1.0 ? 1 : 0) | (c->p.mu_law == HGKS_MU_POWER ? 2 : 0);
+    const dim3 blk(FluxCfg<T>::NT);
+    T* fo = (T*)c->F[d];
+    switch (d * 4 + var) {
+      case 0: flux_kernel<T, 0, STAGE, 0><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 1: flux_kernel<T, 0, STAGE, 1><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 2: flux_kernel<T, 0, STAGE, 2><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 3: flux_kernel<T, 0, STAGE, 3><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 4: flux_kernel<T, 1, STAGE, 0><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 5: flux_kernel<T, 1, STAGE, 1><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 6: flux_kernel<T, 1, STAGE, 2><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 7: flux_kernel<T, 1, STAGE, 3><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 8: flux_kernel<T, 2, STAGE, 0><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 9: flux_kernel<T, 2, STAGE, 1><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      case 10: flux_kernel<T, 2, STAGE, 2><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+      default: flux_kernel<T, 2, STAGE, 3><<<grid, blk, smem, c->s>>>(ff, fo, g, gas, c->ctl, fpb); break;
+    }
     prof_end(c, HGKS_K_FLUX_X + d);
     CUDA_TRY(c, cudaEventRecord(c->ev_flux[d], c->s));
     return HGKS_OK;

@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
 // Lane layout in phase C: lane = 16 n + 2 TT1 bl + TT1 m + a (a = t1 face in tile, (m, n) the Gauss
 // point, t2 face b = BPW w + bl), so every half-warp reads 2 TT1 consecutive (m, a) words of sB from
 // each of its 16 / (2 TT1) rows, in disjoint bank groups.
-template <typename T, int DIR, int STAGE, bool PRF>
+// VAR: bit 0 = PRF (Pr != 1 heat-flux fix, O-12), bit 1 = power-law viscosity
+template <typename T, int DIR, int STAGE, int VAR>
 __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl,
                 int fpb) {
@@ -644,7 +645,8 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     return v;
   };
   const T dt = T(ctl->dt);
-  GpFlux<T, STAGE == 1, PRF> gf;
+  constexpr bool PRF = VAR & 1;
+  GpFlux<T, STAGE == 1, PRF, (VAR >> 1) & 1> gf;
   // value and t2-derivative of Ql, Qr from the same five row loads (the t2 derivatives are held
   // until the side passes: 10 more live registers, 50 fewer shared loads per Gauss point)
   auto tvd = [&](int c, int k, T& v, T& d) {

@@ -15,7 +15,7 @@ txt = subprocess.run(["nvdisasm", "-c", cubin], capture_output=True, text=True).
 parts = re.split(r"\n\s*\.text\.(\S+):", txt)
 for i in range(1, len(parts), 2):
     name, body = parts[i], parts[i + 1]
-    m = re.search(r"flux_kernelI([df])Li(\d)ELi(\d)ELb(\d)", name)
+    m = re.search(r"flux_kernelI([df])Li(\d)ELi(\d)EL[bi](\d)", name)
     if not m:
         continue
     ops = collections.Counter()
