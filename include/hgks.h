@@ -149,6 +149,29 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
  * (a failed peer, see hgks_step).  Synchronises. */
 int hgks_get_state(hgks_ctx* c, double* q, int on_device);
 
+/* Asynchronous host I/O: the per-rank input / output of the run overlapped with the step.
+ * The copies run on a dedicated I/O stream of the context (the GPU's copy engines), so an upload of the
+ * next input and the download of the last result proceed while hgks_step computes.  Buffers (two fp64
+ * states) and the stream are allocated on the first call.  q must be PAGE-LOCKED host memory (pinned;
+ * pageable memory works but the copy is then synchronous) in the hgks_set_state layout, and must stay
+ * valid and untouched until the copy is known complete (below).  All four are collective like every call.
+ *   hgks_upload_state(c, q)   enqueue the host-to-device copy of q into the upload buffer; returns at once.
+ *                             q may be reused after the next hgks_commit_state returns.
+ *   hgks_commit_state(c)      make the last upload the current state: exactly hgks_set_state of it
+ *                             (validity check, first wave speed; synchronises the compute stream; same
+ *                             errors).  HGKS_EINVAL without a pending upload.
+ *   hgks_download_state(c, q) snapshot the current state (ordered after every enqueued step) into the
+ *                             download buffer and enqueue its device-to-host copy to q; returns at once.
+ *                             q holds the state once hgks_io_wait returns; a following hgks_step overlaps
+ *                             the copy.  HGKS_EINVAL without a state.
+ *   hgks_io_wait(c)           wait for every upload and download enqueued so far (HGKS_ECUDA on failure).
+ * A time-marching driver that reads every step's state out and feeds new inputs in thus pays the PCIe
+ * transfers only where they exceed the step (bench.py's e2e loop). */
+int hgks_upload_state(hgks_ctx* c, const double* q);
+int hgks_commit_state(hgks_ctx* c);
+int hgks_download_state(hgks_ctx* c, double* q);
+int hgks_io_wait(hgks_ctx* c);
+
 /* Release everything owned by c (device buffers, streams, events, NCCL communicators; the end of
  * the run of Fig. 3's code frame).  NULL-safe.  Collective like every call: a loopback-group rank
  * waits (host barrier) until every rank of the group has entered hgks_destroy, so no rank frees

@@ -99,6 +99,12 @@ struct hgks_ctx {
   long long graph_launches = 0;             // kernels in one replay (launch accounting)
   void* red_tmp = nullptr;            // loopback reduction result before the in-place write-back
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
+  // asynchronous host I/O (hgks_upload_state / commit / download / io_wait), allocated on first use:
+  // an I/O stream whose copies run on the copy engines beside the step, an upload and a download buffer
+  cudaStream_t sio = nullptr;
+  double *up64 = nullptr, *down64 = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_upfree = nullptr, ev_packed = nullptr, ev_downdone = nullptr;
+  bool up_pending = false;
   Ctl* ctl = nullptr;
   Ctl* ctl_host = nullptr;    // pinned
   int cur = 0;
@@ -1025,11 +1031,11 @@ int hgks_local_extent(const hgks_ctx* c, int32_t* z_begin, int32_t* nz_local) {
 }  // extern "C"
 
 template <typename T>
-static int set_state_t(hgks_ctx* c) {
+static int set_state_t(hgks_ctx* c, const double* src) {
   Geo<T> g = make_geo<T>(c);
   const long long ncell = (long long)g.n[0] * g.n[1] * g.n[2];
   T* Q = (T*)c->Q[c->cur];
-  pack_kernel<T><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>(c->stage64, Q, g);
+  pack_kernel<T><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>(src, Q, g);
   int rc;
   if (c->p.force_mode != HGKS_FORCE_NONE && (rc = diagnostics_t<T>(c))) return rc;  // bulk of Q^0 (O-27)
   Ctl* h = c->ctl_host;
@@ -1079,7 +1085,75 @@ int hgks_set_state(hgks_ctx* c, const double* q, int on_device) {
   CUDA_TRY(c, cudaSetDevice(c->dev));
   size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
   CUDA_TRY(c, cudaMemcpyAsync(c->stage64, q, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
-  return c->fp32 ? set_state_t<float>(c) : set_state_t<double>(c);
+  return c->fp32 ? set_state_t<float>(c, c->stage64) : set_state_t<double>(c, c->stage64);
+}
+
+// ---- asynchronous host I/O (hgks.h: hgks_upload_state .. hgks_io_wait) --------------------------
+static int io_init(hgks_ctx* c) {
+  if (c->sio) return HGKS_OK;
+  const size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
+  bool ok = cudaStreamCreateWithFlags(&c->sio, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->up64, bytes) == cudaSuccess && cudaMalloc(&c->down64, bytes) == cudaSuccess;
+  for (cudaEvent_t* e : {&c->ev_up, &c->ev_upfree, &c->ev_packed, &c->ev_downdone})
+    ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) return fail(c, HGKS_ENOMEM, "asynchronous I/O: stream / buffers / events could not be created");
+  // nothing in flight yet: the 'buffer free' events start recorded
+  CUDA_TRY(c, cudaEventRecord(c->ev_upfree, c->s));
+  CUDA_TRY(c, cudaEventRecord(c->ev_downdone, c->sio));
+  return HGKS_OK;
+}
+
+int hgks_upload_state(hgks_ctx* c, const double* q) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_upload_state: ctx is NULL");
+  if (!q) return fail(c, HGKS_EINVAL, "hgks_upload_state: q is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  int rc;
+  if ((rc = io_init(c))) return rc;
+  const size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
+  CUDA_TRY(c, cudaStreamWaitEvent(c->sio, c->ev_upfree, 0));  // the previous commit has read up64
+  CUDA_TRY(c, cudaMemcpyAsync(c->up64, q, bytes, cudaMemcpyHostToDevice, c->sio));
+  CUDA_TRY(c, cudaEventRecord(c->ev_up, c->sio));
+  c->up_pending = true;
+  return HGKS_OK;
+}
+
+int hgks_commit_state(hgks_ctx* c) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_commit_state: ctx is NULL");
+  if (!c->up_pending) return fail(c, HGKS_EINVAL, "hgks_commit_state: no hgks_upload_state pending");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_up, 0));
+  c->up_pending = false;
+  const int rc = c->fp32 ? set_state_t<float>(c, c->up64) : set_state_t<double>(c, c->up64);
+  CUDA_TRY(c, cudaEventRecord(c->ev_upfree, c->s));
+  return rc;
+}
+
+int hgks_download_state(hgks_ctx* c, double* q) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_download_state: ctx is NULL");
+  if (!q) return fail(c, HGKS_EINVAL, "hgks_download_state: q is NULL");
+  if (!c->have_state) return fail(c, HGKS_EINVAL, "hgks_download_state: no state set");
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  int rc;
+  if ((rc = io_init(c))) return rc;
+  const long long ncell = (long long)c->n[0] * c->n[1] * c->nzl;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s, c->ev_downdone, 0));  // the previous D2H has read down64
+  if (c->fp32) unpack_kernel<float><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>((const float*)c->Q[c->cur], c->down64, make_geo<float>(c));
+  else unpack_kernel<double><<<blocks_for(5 * ncell, 256), 256, 0, c->s>>>((const double*)c->Q[c->cur], c->down64, make_geo<double>(c));
+  c->total_launches += 1;
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaEventRecord(c->ev_packed, c->s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->sio, c->ev_packed, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(q, c->down64, 5 * ncell * sizeof(double), cudaMemcpyDeviceToHost, c->sio));
+  CUDA_TRY(c, cudaEventRecord(c->ev_downdone, c->sio));
+  return HGKS_OK;
+}
+
+int hgks_io_wait(hgks_ctx* c) {
+  if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_io_wait: ctx is NULL");
+  if (!c->sio) return HGKS_OK;
+  CUDA_TRY(c, cudaSetDevice(c->dev));
+  CUDA_TRY(c, cudaStreamSynchronize(c->sio));
+  return HGKS_OK;
 }
 
 int hgks_get_state(hgks_ctx* c, double* q, int on_device) {
@@ -1333,6 +1407,14 @@ int hgks_destroy(hgks_ctx* c) {
     if (c->ev_flux[d]) cudaEventDestroy(c->ev_flux[d]);
   }
   cudaFree(c->stage64);
+  if (c->sio) {
+    cudaStreamSynchronize(c->sio);
+    cudaStreamDestroy(c->sio);
+  }
+  cudaFree(c->up64);
+  cudaFree(c->down64);
+  for (cudaEvent_t e : {c->ev_up, c->ev_upfree, c->ev_packed, c->ev_downdone})
+    if (e) cudaEventDestroy(e);
   cudaFree(c->ctl);
   if (c->ctl_host) cudaFreeHost(c->ctl_host);
   for (int k = 0; k < 2 * 4096; ++k)

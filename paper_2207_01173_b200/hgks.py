@@ -34,7 +34,9 @@ KERNEL_CLASSES = ("flux_x", "flux_y", "flux_z", "update", "ghost", "halo", "dt",
 EXPORTED = ("hgks_create", "hgks_local_extent", "hgks_set_state", "hgks_step", "hgks_get_state",
             "hgks_destroy", "hgks_last_error", "hgks_nccl_id_bytes", "hgks_get_nccl_id",
             "hgks_slab_of", "hgks_make_halo_plan", "hgks_profile_enable", "hgks_profile_read",
-            "hgks_diagnostics", "hgks_history_enable", "hgks_history_read", "hgks_plane_stats", "hgks_get_forcing", "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
+            "hgks_diagnostics", "hgks_history_enable", "hgks_history_read", "hgks_plane_stats", "hgks_get_forcing",
+            "hgks_upload_state", "hgks_commit_state", "hgks_download_state", "hgks_io_wait",
+            "hgks_test_gp_flux", "hgks_test_operator", "hgks_test_face_flux")
 STAT_NAMES = ("rho", "U", "V", "W", "UU", "VV", "WW", "UV", "rhoU", "rhoV", "rhoUV", "c", "M", "MM", "T", "p")
 DIAG_NAMES = ("E_k", "enstrophy", "eps_s", "eps_d", "mass", "mom_x", "mom_y", "mom_z", "energy", "volume",
               "p_dil")
@@ -81,6 +83,10 @@ def lib():
         L.hgks_set_state.argtypes = [vp, vp, C.c_int]
         L.hgks_step.argtypes = [vp, C.c_int32, C.c_double, _dp, _dp]
         L.hgks_get_state.argtypes = [vp, vp, C.c_int]
+        L.hgks_upload_state.argtypes = [vp, vp]
+        L.hgks_commit_state.argtypes = [vp]
+        L.hgks_download_state.argtypes = [vp, vp]
+        L.hgks_io_wait.argtypes = [vp]
         L.hgks_destroy.argtypes = [vp]
         L.hgks_last_error.restype = C.c_char_p
         L.hgks_last_error.argtypes = [vp]
@@ -196,6 +202,37 @@ def hgks_set_state(ctx, q) -> None:
 def hgks_get_state(ctx, q) -> None:
     p, dev = _ptr(q)
     _check(lib().hgks_get_state(ctx, p, dev), ctx)
+
+
+def _host_ptr(q) -> int:
+    """Address of a C-contiguous float64 HOST buffer (numpy array or CPU torch tensor, ideally pinned)."""
+    if isinstance(q, np.ndarray):
+        if q.dtype != np.float64 or not q.flags["C_CONTIGUOUS"]:
+            raise TypeError("state must be C-contiguous float64")
+        return q.ctypes.data
+    import torch  # noqa: PLC0415
+    if not isinstance(q, torch.Tensor) or q.dtype != torch.float64 or not q.is_contiguous() or q.is_cuda:
+        raise TypeError("asynchronous I/O needs a contiguous float64 host tensor (pinned for overlap)")
+    return q.data_ptr()
+
+
+def hgks_upload_state(ctx, q) -> None:
+    """Enqueue the H2D copy of host state q (keep q alive until the next hgks_commit_state)."""
+    _check(lib().hgks_upload_state(ctx, _host_ptr(q)), ctx)
+
+
+def hgks_commit_state(ctx) -> None:
+    """Make the last upload the current state (= hgks_set_state of it)."""
+    _check(lib().hgks_commit_state(ctx), ctx)
+
+
+def hgks_download_state(ctx, q) -> None:
+    """Enqueue the D2H copy of the current state into host buffer q (valid after hgks_io_wait)."""
+    _check(lib().hgks_download_state(ctx, _host_ptr(q)), ctx)
+
+
+def hgks_io_wait(ctx) -> None:
+    _check(lib().hgks_io_wait(ctx), ctx)
 
 
 def hgks_step(ctx, nsteps: int, t: float = 0.0, t_end: float = 0.0):
@@ -346,6 +383,20 @@ class Solver:
             out = np.zeros(self.local_shape)
         hgks_get_state(self.ctx, out)
         return out
+
+    # asynchronous host I/O overlapped with the steps (hgks.h: hgks_upload_state .. hgks_io_wait)
+    def upload_state(self, q):
+        hgks_upload_state(self.ctx, q)
+
+    def commit_state(self, t: float = 0.0):
+        hgks_commit_state(self.ctx)
+        self.t = t
+
+    def download_state(self, out):
+        hgks_download_state(self.ctx, out)
+
+    def io_wait(self):
+        hgks_io_wait(self.ctx)
 
     def close(self):
         if self.ctx:
