@@ -1,4 +1,4 @@
-"""Turn the ncu counter CSVs of tools/gpu_profile_round.sh into profiles/ summaries.
+"""Turn the ncu counter CSVs of tools/gpu_counters_round.sh into profiles/ summaries.
 
 usage: python tools/counters_to_profile.py TAG N   (N = grid n of the profiled run, 256)
 Writes profiles/flux_flops.json (read by bench.py for roofline.achieved / traffic) and
@@ -28,7 +28,7 @@ def faces(kname, n):
 
 
 def main(tag, n):
-    out = {"source": f"ncu SASS counters (tools/gpu_profile_round.sh {tag}), TGV {n}^3", "grid": n}
+    out = {"source": f"ncu SASS counters (tools/gpu_counters_round.sh {tag}), TGV {n}^3", "grid": n}
     md = [f"# Kernel counters, round tag `{tag}` (TGV {n}^3, one step, ncu --clock-control none)\n",
           "| precision | kernel | time ms | FP64 flop (DFMA*2+DMUL+DADD) | FP32 flop | flop/face | FP64 pipe % | DRAM read MB | DRAM write MB |",
           "|---|---|---|---|---|---|---|---|---|"]

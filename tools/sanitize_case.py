@@ -27,6 +27,15 @@ if mode == "single":
             H.hgks_history_read(s.ctx, 8)
             s.diagnostics()
             s.get_state()
+            # asynchronous host I/O: upload / commit / step / download overlapping, io_wait
+            out = np.zeros_like(q)
+            s.upload_state(q)
+            s.commit_state()
+            s.upload_state(q)
+            s.step(1)
+            s.download_state(out)
+            s.commit_state()
+            s.io_wait()
     print("single ok")
 elif mode == "ragged":
     grid = (21, 18, 23)
