@@ -101,12 +101,14 @@ struct hgks_ctx {
   double* stage64 = nullptr;  // fp64 [5][nzl][ny][nx] staging for set/get
   // asynchronous host I/O (hgks_upload_state / commit / download / io_wait), allocated on first use:
   // an I/O stream whose copies run on the copy engines beside the step, an upload and a download buffer
-  cudaStream_t sio = nullptr;
+  cudaStream_t sio = nullptr, sio_up = nullptr;  // downloads (device -> host) / uploads (host -> device):
+                                                 // one stream per direction, so PCIe runs both at once
   double *up64 = nullptr, *down64 = nullptr;
   cudaEvent_t ev_up = nullptr, ev_upfree = nullptr, ev_packed = nullptr, ev_downdone = nullptr;
   bool up_pending = false;
   Ctl* ctl = nullptr;
-  Ctl* ctl_host = nullptr;    // pinned
+  Ctl* ctl_host = nullptr;    // pinned, mapped
+  Ctl* ctl_host_dev = nullptr;  // device alias of ctl_host
   int cur = 0;
   bool have_state = false;
   cudaStream_t s = nullptr;
@@ -184,6 +186,21 @@ static int sync_s(hgks_ctx* c) {
   do {                           \
     const int rc_ = sync_s(c);   \
     if (rc_) return rc_;         \
+  } while (0)
+
+// control block -> its mapped host copy (one block, 8-byte words, made visible to the host before the
+// kernel completes); the caller synchronises the stream before reading c->ctl_host
+__global__ void ctl_readback_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src) {
+  for (int i = threadIdx.x; i < (int)(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+static_assert(sizeof(Ctl) % 8 == 0, "Ctl copied as 8-byte words");
+#define CTL_READBACK(c)                                                                                   \
+  do {                                                                                                    \
+    ctl_readback_kernel<<<1, 32, 0, (c)->s>>>((unsigned long long*)(c)->ctl_host_dev,                      \
+                                              (const unsigned long long*)(c)->ctl);                      \
+    (c)->total_launches += 1;                                                                             \
+    CUDA_TRY(c, cudaGetLastError());                                                                      \
   } while (0)
 
 // ---- instrumentation ------------------------------------------------------------------------
@@ -975,7 +992,10 @@ int hgks_create(const hgks_params* p, hgks_ctx** out) {
     free(h);
   }
   ok = ok && cudaMalloc(&c->ctl, sizeof(Ctl)) == cudaSuccess;
-  ok = ok && cudaMallocHost(&c->ctl_host, sizeof(Ctl)) == cudaSuccess;
+  // the host copy of the control block is MAPPED pinned memory: readbacks are a one-block kernel writing
+  // over PCIe, not a copy-engine transfer that would queue behind an in-flight multi-100-MB state download
+  ok = ok && cudaHostAlloc((void**)&c->ctl_host, sizeof(Ctl), cudaHostAllocMapped) == cudaSuccess &&
+       cudaHostGetDevicePointer((void**)&c->ctl_host_dev, c->ctl_host, 0) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     fail(c, HGKS_ENOMEM, "device allocation failed");
@@ -1039,7 +1059,7 @@ static int set_state_t(hgks_ctx* c, const double* src) {
   int rc;
   if (c->p.force_mode != HGKS_FORCE_NONE && (rc = diagnostics_t<T>(c))) return rc;  // bulk of Q^0 (O-27)
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   if (c->p.force_mode != HGKS_FORCE_NONE) {  // restart the controller from this state
     const double* a = c->diag_host;
@@ -1059,7 +1079,7 @@ static int set_state_t(hgks_ctx* c, const double* src) {
   c->total_launches += 2;
   CUDA_TRY(c, cudaGetLastError());
   if ((rc = coll_allreduce(c, &c->ctl->red[0], 2, 0))) return rc;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   if (h->red[1]) {
     if (h->bad_cell != ~0ull) {
@@ -1092,7 +1112,8 @@ int hgks_set_state(hgks_ctx* c, const double* q, int on_device) {
 static int io_init(hgks_ctx* c) {
   if (c->sio) return HGKS_OK;
   const size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
-  bool ok = cudaStreamCreateWithFlags(&c->sio, cudaStreamNonBlocking) == cudaSuccess;
+  bool ok = cudaStreamCreateWithFlags(&c->sio, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->sio_up, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaMalloc(&c->up64, bytes) == cudaSuccess && cudaMalloc(&c->down64, bytes) == cudaSuccess;
   for (cudaEvent_t* e : {&c->ev_up, &c->ev_upfree, &c->ev_packed, &c->ev_downdone})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
@@ -1110,9 +1131,9 @@ int hgks_upload_state(hgks_ctx* c, const double* q) {
   int rc;
   if ((rc = io_init(c))) return rc;
   const size_t bytes = 5 * (size_t)c->n[0] * c->n[1] * c->nzl * sizeof(double);
-  CUDA_TRY(c, cudaStreamWaitEvent(c->sio, c->ev_upfree, 0));  // the previous commit has read up64
-  CUDA_TRY(c, cudaMemcpyAsync(c->up64, q, bytes, cudaMemcpyHostToDevice, c->sio));
-  CUDA_TRY(c, cudaEventRecord(c->ev_up, c->sio));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->sio_up, c->ev_upfree, 0));  // the previous commit has read up64
+  CUDA_TRY(c, cudaMemcpyAsync(c->up64, q, bytes, cudaMemcpyHostToDevice, c->sio_up));
+  CUDA_TRY(c, cudaEventRecord(c->ev_up, c->sio_up));
   c->up_pending = true;
   return HGKS_OK;
 }
@@ -1152,6 +1173,7 @@ int hgks_io_wait(hgks_ctx* c) {
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_io_wait: ctx is NULL");
   if (!c->sio) return HGKS_OK;
   CUDA_TRY(c, cudaSetDevice(c->dev));
+  CUDA_TRY(c, cudaStreamSynchronize(c->sio_up));
   CUDA_TRY(c, cudaStreamSynchronize(c->sio));
   return HGKS_OK;
 }
@@ -1183,7 +1205,7 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
   if (c->hist_cap > 0) c->hist_pending += nsteps;
   // reset per-call control: t, t_end, counters (one small H2D copy)
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   h->t = *t_inout;
   h->t_end = t_end;
@@ -1201,7 +1223,7 @@ int hgks_step(hgks_ctx* c, int32_t nsteps, double t_end, double* t_inout, double
     const int n = std::min(chunk, nsteps - done);
     int rc = c->fp32 ? run_steps_graphed<float>(c, n) : run_steps_graphed<double>(c, n);
     if (rc) return rc;
-    CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+    CTL_READBACK(c);
     SYNC_TRY(c);
     if (h->halt || n <= 0) break;
   }
@@ -1239,7 +1261,7 @@ static void normalise_diag(const hgks_ctx* c, double rho0, const double* a, doub
 
 static int set_ctl_hist(hgks_ctx* c, int n, int cap) {
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   h->hist_n = n;
   h->hist_cap = cap;
@@ -1292,7 +1314,7 @@ int hgks_history_read(hgks_ctx* c, double* out, int32_t max_rows, int32_t* rows)
   if (c->hist_cap <= 0) return fail(c, HGKS_EINVAL, "hgks_history_read: history not enabled");
   CUDA_TRY(c, cudaSetDevice(c->dev));
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   const int n = h->hist_n;
   if (n > max_rows || (n > 0 && !out))
@@ -1362,7 +1384,7 @@ int hgks_get_forcing(hgks_ctx* c, double* force, double* bulk_momentum, double* 
   if (!c) return fail(nullptr, HGKS_EINVAL, "hgks_get_forcing: ctx is NULL");
   CUDA_TRY(c, cudaSetDevice(c->dev));
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   const bool b = c->p.force_mode == HGKS_FORCE_BULK;
   if (force) *force = h->f_prev;
@@ -1407,9 +1429,11 @@ int hgks_destroy(hgks_ctx* c) {
     if (c->ev_flux[d]) cudaEventDestroy(c->ev_flux[d]);
   }
   cudaFree(c->stage64);
-  if (c->sio) {
-    cudaStreamSynchronize(c->sio);
-    cudaStreamDestroy(c->sio);
+  for (cudaStream_t st : {c->sio, c->sio_up}) {
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
   }
   cudaFree(c->up64);
   cudaFree(c->down64);
@@ -1493,7 +1517,7 @@ static int test_operator_t(hgks_ctx* c, double dt, double* L, double* dL) {
   Geo<T> g = make_geo<T>(c);
   T* Q = (T*)c->Q[c->cur];
   Ctl* h = c->ctl_host;
-  CUDA_TRY(c, cudaMemcpyAsync(h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->s));
+  CTL_READBACK(c);
   SYNC_TRY(c);
   h->dt = dt;
   h->idt = 1.0 / dt;
