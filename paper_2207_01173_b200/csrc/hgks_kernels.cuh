@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
 template <typename T, int DIR, int STAGE, int VAR>
 __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     flux_kernel(const T* __restrict__ ff, T* __restrict__ flux, Geo<T> g, GasK<T> gas, const Ctl* __restrict__ ctl,
-                int fpb) {
+                int jofs) {
   if (ctl->halt) return;
   constexpr int A1 = (DIR + 1) % 3, A2 = (DIR + 2) % 3;  // tangent axes t1, t2 (O-23)
   using Cfg = FluxCfg<T>;
@@ -448,14 +448,14 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   T* sB = sA + 6 * 5 * SA_C;               // t1-pass outputs (FluxCfg: RS, CS, KS, MA)
 
   const int n1 = g.n[A1], n2 = g.n[A2];
-  const int t10 = blockIdx.x * TT1, t20 = blockIdx.y * TT2;
+  // jofs: first t2 tile of this launch (the x sweep's tiles run in parts as their face-field lines land)
+  const int t10 = blockIdx.x * TT1, t20 = (blockIdx.y + jofs) * TT2;
   // fpb consecutive normal faces per block: the face fields of face fn+1 are copied
   // (cp.async) into sA while face fn is in phase C, so only the first copy's latency is exposed
   // gridDim.z blocks share the n+1 normal faces as evenly as possible (fpb or fpb - 1 each)
   const int nf_all = g.n[DIR] + 1;
   const int fn0 = (int)(((long long)blockIdx.z * nf_all) / gridDim.z);
   const int nfn = (int)(((long long)(blockIdx.z + 1) * nf_all) / gridDim.z) - fn0;
-  (void)fpb;
   auto issue_A = [&](int fn) {
     const FFLayout<T, DIR> L = ff_layout<T, DIR>(g);
     const long long fstride = (long long)L.nf * L.nl;  // next (field, component)
