@@ -327,7 +327,12 @@ def measure_rank(args, env) -> dict | None:
     for prec_name, prec in (("fp64", H.HGKS_FP64), ("fp32", H.HGKS_FP32)):
         if (prec_name == "fp32" and args.no_fp32) or (prec_name == "fp64" and args.only_fp32):
             continue
+        torch.cuda.synchronize(env.device)
+        free0 = torch.cuda.mem_get_info(env.device)[0]
         s = make_solver(prec)
+        torch.cuda.synchronize(env.device)
+        # device memory the library allocated for this context (Table 8's "memory cost")
+        mem_bytes = free0 - torch.cuda.mem_get_info(env.device)[0]
         if ws > 1:  # evidence of the N-rank launch for the driver's log (stderr; stdout is the JSON line)
             print(f"[bench] {prec_name}: rank {rank}/{ws} on cuda:{env.device}, transport {env.transport}, "
                   f"z-slab [{s.z0}, {s.z0 + s.nz_local}) of {grid[2]}", file=sys.stderr, flush=True)
@@ -353,7 +358,7 @@ def measure_rank(args, env) -> dict | None:
         cells = grid[0] * grid[1] * grid[2]
         rate = cells * args.steps / (ms / 1000.0)
         res = dict(ms_per_step=ms / args.steps, value=rate, clocks=clk.summary(), ms_k=ms_k, launches=launches,
-                   total_launches=total_launches, t=s.t)
+                   total_launches=total_launches, t=s.t, mem_bytes=int(env.reduce(float(mem_bytes), "sum")))
         # NEXT-1/2 device reductions outside the timed step (synchronous calls, events on the stream)
         aux = {}
         for name, fn in (("diagnostics", lambda: H.hgks_diagnostics(s.ctx)),
@@ -499,8 +504,14 @@ def report(args, out, ws, transport):
     if "e2e" in r64:
         line["e2e"] = r64["e2e"]
         line["e2e_sync"] = r64.get("e2e_sync")
+    cells = grid[0] * grid[1] * grid[2]
+    line["memory"] = {"fp64_bytes": r64["mem_bytes"], "fp64_bytes_per_cell": r64["mem_bytes"] / cells,
+                      "note": "device memory allocated by hgks_create (cudaMemGetInfo delta), all ranks; Table 8's "
+                              "memory cost (P:1043-1071)"}
     if "fp32" in results:
         r32 = results["fp32"]
+        line["memory"].update({"fp32_bytes": r32["mem_bytes"], "fp32_bytes_per_cell": r32["mem_bytes"] / cells,
+                               "R_fp": r64["mem_bytes"] / max(1, r32["mem_bytes"])})
         line["fp32"] = {"value": r32["value"], "ms_per_step": r32["ms_per_step"], "clocks": r32["clocks"],
                         "e2e": r32.get("e2e"), "e2e_sync": r32.get("e2e_sync"),
                         "speedup_vs_fp64": r32["value"] / r64["value"],
