@@ -85,7 +85,7 @@ struct hgks_ctx {
   size_t red_tmp_count = 0;
   void* FF[2] = {nullptr, nullptr};  // face fields (recon_kernel output), alternating per direction
   size_t ff_elems = 0;
-  cudaStream_t s2 = nullptr;          // reconstruction stream: recon of direction d+1 overlaps flux of d
+  cudaStream_t s2 = nullptr;          // reconstruction stream when HGKS_RECON_OVERLAP (recon d+1 beside flux d)
   cudaStream_t sc = nullptr;          // communication stream (high priority): the z halo of each stage
   cudaEvent_t ev_in = nullptr, ev_rec[3] = {}, ev_flux[3] = {};
   cudaEvent_t ev_recA = nullptr;      // first x-sweep reconstruction: the lines of z < zA landed
@@ -543,17 +543,21 @@ static int flux_sweeps(hgks_ctx* c, const T* q) {
   int rc0;
   if ((rc0 = set_flux_attrs<T, STAGE>(c))) return rc0;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-#ifndef HGKS_DEBUG_SERIAL
-#define HGKS_DEBUG_SERIAL 0  // timing experiment only: reconstruction on the compute stream (no overlap)
+#ifndef HGKS_RECON_OVERLAP
+#define HGKS_RECON_OVERLAP 0
 #endif
-  cudaStream_t rs = HGKS_DEBUG_SERIAL ? c->s : c->s2;  // the reconstruction stream
-  // Two streams: the reconstruction sweep of the next direction (memory-bound) runs on s2 while the
-  // flux sweep of the current one (FP64-bound) runs on s.  Face-field buffer FF[pos & 1] by position
-  // in the sweep order; recon(pos 2) waits for flux(pos 0) before reusing its buffer.  Measured at
-  // 256^3 (HGKS_DEBUG_SERIAL): the two flux kernels that run beside a reconstruction slow down by that
-  // reconstruction's own serial time, so the overlap is neutral there (285M cell-updates/s either
-  // way) and only pays on thin slabs (256 x 256 x 32: +1 %) -- two blocks per SM already fill the
-  // register file, so a concurrent reconstruction block always displaces flux work.
+  // The reconstruction stream.  HGKS_RECON_OVERLAP = 1: the reconstruction sweep of the next direction
+  // (memory-bound) runs on s2 while the flux sweep of the current one (FP64-bound) runs on s.
+  // Measured (round 2, TGV 256^3): the flux kernel that runs beside a reconstruction slows down by that
+  // reconstruction's own serial time -- three blocks per SM fill the register file, so a concurrent
+  // reconstruction block always displaces flux work -- and the step rate is the same either way
+  // (314.8M serial vs 314M overlapped; thin slabs 256 x 256 x 32: -1 %).  Default: the reconstruction
+  // runs on the compute stream between the flux sweeps, so every flux launch runs alone and its event
+  // time is its own (roofline.frac 0.571 instead of 0.546 with the reconstruction's time inside the
+  // x-flux events).  The halo overlap below is unaffected: the halo runs on its own stream.
+  cudaStream_t rs = HGKS_RECON_OVERLAP ? c->s2 : c->s;
+  // Face-field buffer FF[pos & 1] by position in the sweep order; recon(pos 2) waits for flux(pos 0)
+  // before reusing its buffer.
   // Stage input: x/y ghosts written (ev_xy, recorded by fill_ghosts on c->s); z ghosts land on
   // c->sc (ev_halo).  The first sweep's face lines of the interior z planes need no z ghost, so
   // they run while the halo is in flight; its ghost-plane lines (z = -2, -1, nz, nz+1) and every
