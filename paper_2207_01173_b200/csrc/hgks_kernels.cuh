@@ -901,12 +901,15 @@ __device__ __forceinline__ void block_max_commit(double s, unsigned long long* d
 constexpr int UPD_X = 64, UPD_Y = DIAG_TPB / UPD_X;  // update_kernel block shape (DIAG_TPB threads)
 // stage-1 update with the per-step history: block shape of its own (HGKS_UPDD_X = 32 -> 32 x 8 cells, a
 // 36 x 12 velocity tile instead of 68 x 8, measured 0.565 vs 0.525 ms/step of history at 256^3: kept 64)
+#ifndef HGKS_UPD2_MINB
+#define HGKS_UPD2_MINB 1  // min blocks per SM of the stage-2 update (occupancy experiment)
+#endif
 #ifndef HGKS_UPDD_X
 #define HGKS_UPDD_X 64
 #endif
 constexpr int UPDD_X = HGKS_UPDD_X, UPDD_Y = DIAG_TPB / UPDD_X;
 template <typename T, int STAGE, bool DIAG = false>
-__global__ void __launch_bounds__(DIAG_TPB) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
+__global__ void __launch_bounds__(DIAG_TPB, (STAGE == 2 && !DIAG) ? HGKS_UPD2_MINB : 1) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
                               Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk,
                               double* __restrict__ dpart = nullptr) {
