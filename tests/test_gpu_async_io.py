@@ -85,3 +85,35 @@ def test_async_io_errors():
             s.commit_state()
         assert e.value.code == H.HGKS_ESTATE and "(6,5,4)" in str(e.value)
         s.io_wait()
+
+
+def test_async_io_loopback_two_ranks():
+    """The asynchronous calls on a 2-slab decomposition (loopback group, one GPU): hgks_commit_state is
+    collective (the first wave speed is allreduced), each rank uploads / downloads its own slab; the
+    gathered result equals the single-domain synchronous run bitwise."""
+    q, _ = inputs.perturbed(GRID, seed=21, amp=0.06)
+    with H.Solver(GRID, (0.0,) * 3, (2 * math.pi,) * 3, **KW) as s:
+        s.set_state(q)
+        s.step(2)
+        ref = s.get_state()
+
+    def work(rank, nranks, key):
+        with H.Solver(GRID, (0.0,) * 3, (2 * math.pi,) * 3, rank=rank, nranks=nranks, group_key=key, **KW) as r:
+            local = np.ascontiguousarray(q[:, r.z0:r.z0 + r.nz_local])
+            inp, out = _pinned(local), _pinned(np.zeros_like(local))
+            r.upload_state(inp)
+            r.commit_state()
+            r.step(1)
+            r.upload_state(inp)  # next input while nothing else is pending: re-commit the same state
+            r.download_state(out)
+            r.io_wait()
+            mid = out.numpy().copy()
+            r.set_state(mid)     # continue from the downloaded state: 1 + 1 steps
+            r.step(1)
+            r.download_state(out)
+            r.io_wait()
+            return r.z0, out.numpy().copy()
+
+    parts = H.run_loopback_group(2, work)
+    got = np.concatenate([p for _, p in sorted(parts, key=lambda t: t[0])], axis=1)
+    assert np.array_equal(got, ref), np.abs(got - ref).max()
