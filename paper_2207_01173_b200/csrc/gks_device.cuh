@@ -102,6 +102,9 @@ __host__ __device__ __forceinline__ double half_erfc(double x) {
 #ifndef HGKS_SERIES_EXP
 #define HGKS_SERIES_EXP 2
 #endif
+#ifndef HGKS_H0_FAST
+#define HGKS_H0_FAST 1
+#endif
 #ifndef HGKS_SERIES_SHORT
 #define HGKS_SERIES_SHORT 1
 #endif
@@ -544,14 +547,28 @@ struct GpFlux {
   HD void finish_gamma() {
     // h = exp(-dt/(2 tau)); tau = 0 -> h = 0 (O-10)
     // (below 1e-20 -- dt/tau > 92, e.g. every low-Mach TGV face -- h changes no Gamma above rounding)
-    const T harg = -T(0.5) * dt * rcp(tau);
-    const bool need_h = tau > T(0) && harg > T(-46);
 #ifdef __CUDA_ARCH__
     // warp-uniform skip: at low Mach every lane of a warp has dt/tau > 92 (h = 0), and the exp is
-    // ~25 FP64 instructions per Gauss point
+    // ~25 FP64 instructions per Gauss point.  HGKS_H0_FAST: the test needs no reciprocal of tau, and with
+    // h = 0 the shared factors reduce to c13 = 3/dt, hb = 0, gp1 = 4 tau/dt^2, gp2 = -8 tau^2/dt^2
+    const bool need_h = tau > T(0) && (HGKS_H0_FAST ? dt < T(92) * tau : -T(0.5) * dt * rcp(tau) > T(-46));
+    const bool any_h = __any_sync(__activemask(), need_h);
+    if (HGKS_H0_FAST && HGKS_GSHARE && !any_h) {
+      h = T(0);
+      const T idt2 = idt * idt;
+      tc13 = T(3) * tau * idt;
+      ttc13 = tau * tc13;
+      hb = T(0);
+      gp1 = T(4) * tau * idt2;
+      gp2 = -T(8) * tau * tau * idt2;
+      tgp1 = tau * gp1;
+      return;
+    }
     h = T(0);
-    if (__any_sync(__activemask(), need_h)) h = need_h ? m_exp(harg) : T(0);
+    if (any_h) h = need_h ? m_exp(-T(0.5) * dt * rcp(tau)) : T(0);
 #else
+    const T harg = -T(0.5) * dt * rcp(tau);
+    const bool need_h = tau > T(0) && harg > T(-46);
     h = need_h ? m_exp(harg) : T(0);
 #endif
     if (HGKS_GSHARE) {
