@@ -538,45 +538,72 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   // Item order: TT1 = 8: (a, c, l2), a half-warp reads 2 components of one row; TT1 = 4: (a, l2, c),
   // a half-warp reads 4 rows (TL1P apart) of one component -- conflict-free (TT1 = 8 except where a
   // warp straddles two rows).
-  for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
-    const int a = w % TT1;
-    const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
-    const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
-    T o0[NB], o1[NB];
+#ifndef HGKS_PB2
+#define HGKS_PB2 0  // phase B: the (up to) two items of a thread accumulated tap by tap together (ILP)
+#endif
+#ifndef HGKS_PB2_FENCE
+#define HGKS_PB2_FENCE 1
+#endif
+  constexpr int NITEM = TT1 * 5 * TL2;
+  constexpr int NPB = HGKS_PB2 ? (NITEM + NTHREADS_FLUX - 1) / NTHREADS_FLUX : 1;
+  for (int w0 = threadIdx.x; do_ab && w0 < NITEM; w0 += NPB * NTHREADS_FLUX) {
+    T o0[NPB][NB], o1[NPB][NB];
+    const T* srcp[NPB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      o0[k] = T(0);
-      o1[k] = T(0);
+    for (int p = 0; p < NPB; ++p) {
+      const int w = min(w0 + p * NTHREADS_FLUX, NITEM - 1);  // a thread without a second item repeats its last
+      const int a = w % TT1;
+      const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
+      const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
+      srcp[p] = sA + c * SA_C + l2 * TL1P + a;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        o0[p][k] = T(0);
+        o1[p][k] = T(0);
+      }
     }
-    const T* src = sA + c * SA_C + l2 * TL1P + a;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
       const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
       const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
+      if (HGKS_PB2_FENCE) asm volatile("" ::: "memory");  // loads of one tap at a time (register pressure)
 #pragma unroll
-      for (int ff = 0; ff < 6; ++ff) {
-        const T x = src[ff * 5 * SA_C + r];
-        o0[ff] += wv0 * x;
-        o1[ff] += wv1 * x;
-        if (ff == 0) { o0[6] += wd0 * x; o1[6] += wd1 * x; }
-        if (ff == 1) { o0[7] += wd0 * x; o1[7] += wd1 * x; }
-        if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
+      for (int p = 0; p < NPB; ++p) {
+#pragma unroll
+        for (int ff = 0; ff < 6; ++ff) {
+          const T x = srcp[p][ff * 5 * SA_C + r];
+          o0[p][ff] += wv0 * x;
+          o1[p][ff] += wv1 * x;
+          if (ff == 0) { o0[p][6] += wd0 * x; o1[p][6] += wd1 * x; }
+          if (ff == 1) { o0[p][7] += wd0 * x; o1[p][7] += wd1 * x; }
+          if (ff == 4) { o0[p][8] += wd0 * x; o1[p][8] += wd1 * x; }
+        }
       }
     }
+#pragma unroll
+    for (int p = 0; p < NPB; ++p) {
+    const int w = w0 + p * NTHREADS_FLUX;
+    if (w >= NITEM) break;
+    const int a = w % TT1;
+    const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
+    const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
+    const T (&o0p)[NB] = o0[p];
+    const T (&o1p)[NB] = o1[p];
     T* dst = sB + l2 * RS + (Cfg::VEC ? 0 : c * CS + Cfg::MA(0, a));
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       if constexpr (Cfg::VEC) {
-        dst[k * KS + Cfg::VOFF(c, Cfg::MA(0, a))] = o0[k];
-        dst[k * KS + Cfg::VOFF(c, Cfg::MA(1, a))] = o1[k];
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(0, a))] = o0p[k];
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(1, a))] = o1p[k];
       } else if constexpr (TT1 == 4 && sizeof(T) == 8) {  // (m = 0, m = 1) adjacent: one 16-byte store
-        *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0[k], (double)o1[k]);
+        *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0p[k], (double)o1p[k]);
       } else if constexpr (TT1 == 4) {
-        *reinterpret_cast<float2*>(dst + k * KS) = make_float2((float)o0[k], (float)o1[k]);
+        *reinterpret_cast<float2*>(dst + k * KS) = make_float2((float)o0p[k], (float)o1p[k]);
       } else {
-        dst[k * KS] = o0[k];
-        dst[k * KS + Cfg::MA(1, 0)] = o1[k];
+        dst[k * KS] = o0p[k];
+        dst[k * KS + Cfg::MA(1, 0)] = o1p[k];
       }
+    }
     }
   }
   if (do_ab) {
