@@ -931,12 +931,15 @@ constexpr int UPD_X = 64, UPD_Y = DIAG_TPB / UPD_X;  // update_kernel block shap
 #ifndef HGKS_UPD2_MINB
 #define HGKS_UPD2_MINB 1  // min blocks per SM of the stage-2 update (occupancy experiment)
 #endif
+#ifndef HGKS_UPD1_MINB
+#define HGKS_UPD1_MINB 2  // min blocks per SM of the stage-1 update without the history (128 registers: 1.88 -> 1.66 ms/step)
+#endif
 #ifndef HGKS_UPDD_X
 #define HGKS_UPDD_X 64
 #endif
 constexpr int UPDD_X = HGKS_UPDD_X, UPDD_Y = DIAG_TPB / UPDD_X;
 template <typename T, int STAGE, bool DIAG = false>
-__global__ void __launch_bounds__(DIAG_TPB, (STAGE == 2 && !DIAG) ? HGKS_UPD2_MINB : 1) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
+__global__ void __launch_bounds__(DIAG_TPB, (STAGE == 2 && !DIAG) ? HGKS_UPD2_MINB : (DIAG ? 1 : HGKS_UPD1_MINB)) update_kernel(const T* __restrict__ Q, T* __restrict__ Qs, T* __restrict__ R,
                               const T* __restrict__ FX, const T* __restrict__ FY, const T* __restrict__ FZ,
                               Geo<T> g, DiagGeo dg, double gamma, Ctl* __restrict__ ctl, double* __restrict__ bulk,
                               double* __restrict__ dpart = nullptr) {
@@ -986,12 +989,18 @@ __global__ void __launch_bounds__(DIAG_TPB, (STAGE == 2 && !DIAG) ? HGKS_UPD2_MI
         R[qi] = q[c] + tdt * L[c] + (T(1) / T(6)) * tdt * tdt * dL[c];
       }
     } else {
+      // R of all five components loaded before the first store: the in-place update R[qi] = ... would
+      // otherwise order each component's load after the previous component's store (R may alias
+      // itself), five dependent DRAM round trips per thread (ncu: long-scoreboard 13 stalls per issue)
+      T r5[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) r5[c] = R[qidx(g, c, i, j, k)];
       if (fmode) {  // O-26: Lt = L + dt/2 dL of Q^n = (8a - 3b)/dt
         const double f = ctl->force;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const long long qi = qidx(g, c, i, j, k);
-          const double qn = (double)Q[qi], a = (double)Qs[qi] - qn, b = (double)R[qi] - qn;
+          const double qn = (double)Q[qi], a = (double)Qs[qi] - qn, b = (double)r5[c] - qn;
           dL[c == 0 ? 1 : 4] += T(f * (8.0 * a - 3.0 * b) / dt);
         }
       }
@@ -999,7 +1008,7 @@ __global__ void __launch_bounds__(DIAG_TPB, (STAGE == 2 && !DIAG) ? HGKS_UPD2_MI
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         const long long qi = qidx(g, c, i, j, k);
-        const T v = R[qi] + (T(1) / T(3)) * tdt * tdt * dL[c];
+        const T v = r5[c] + (T(1) / T(3)) * tdt * tdt * dL[c];
         R[qi] = v;
         out[c] = v;
       }
