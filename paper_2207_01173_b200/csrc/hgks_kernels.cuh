@@ -310,6 +310,11 @@ __device__ __forceinline__ FFLayout<T, DIR> ff_layout(const Geo<T>& g) {
   return L;
 }
 
+#ifndef HGKS_RC_PF
+#define HGKS_RC_PF 1  // cells of the reconstruction march prefetched ahead (1: one, the loop's own)
+#endif
+constexpr int RC_PF = HGKS_RC_PF;
+
 // Subset of the face lines of one sweep: lines lbeg + j for j in [0, lcnt), where j >= gap_at
 // skips ahead by gap (two disjoint ranges in one launch: the ghost-plane lines of the x sweep).
 struct LineRange {
@@ -350,9 +355,17 @@ __global__ void __launch_bounds__(128) recon_kernel(const T* __restrict__ q, T* 
   const int nf = L.nf;
   const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
   T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
-  T Ap = T(0), Bp = T(0);  // edges of cell fn-1
+  T Ap = T(0), Bp = T(0);
+  // software prefetch: the next RC_PF cells of the march are in flight while cell fn is reconstructed
+  // (window index fn + 5 of the march ends at fe + 4, the last ghost layer)
+  T pf[RC_PF];
+#pragma unroll
+  for (int k = 0; k < RC_PF; ++k) pf[k] = (fs + 4 + k <= fe + 4) ? p[(fs + 4 + k) * sN] : T(0);  // edges of cell fn-1
   for (int fn = fs - 1; fn < fe; ++fn) {
-    s5 = p[(fn + 5) * sN];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
+    s5 = pf[0];  // Qbar_{fn+2}; window s1..s5 = Qbar_{fn-2..fn+2}
+#pragma unroll
+    for (int k = 0; k + 1 < RC_PF; ++k) pf[k] = pf[k + 1];
+    pf[RC_PF - 1] = (fn + 5 + RC_PF <= fe + 4) ? p[(fn + 5 + RC_PF) * sN] : T(0);
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);  // cell fn
     if (fn >= fs) {
@@ -402,8 +415,16 @@ __global__ void __launch_bounds__(RZ_Z * RZ_X) recon_yz_kernel(const T* __restri
   const int fs = (int)(((long long)seg * nf) / nseg), fe = (int)(((long long)(seg + 1) * nf) / nseg);
   T s1v = p[fs * sN], s2v = p[(fs + 1) * sN], s3 = p[(fs + 2) * sN], s4 = p[(fs + 3) * sN], s5;
   T Ap = T(0), Bp = T(0);
+  // software prefetch: the next RC_PF cells of the march are in flight while cell fn is reconstructed
+  // (window index fn + 5 of the march ends at fe + 4, the last ghost layer)
+  T pf[RC_PF];
+#pragma unroll
+  for (int k = 0; k < RC_PF; ++k) pf[k] = (fs + 4 + k <= fe + 4) ? p[(fs + 4 + k) * sN] : T(0);
   for (int fn = fs - 1; fn < fe; ++fn) {
-    s5 = p[(fn + 5) * sN];
+    s5 = pf[0];
+#pragma unroll
+    for (int k = 0; k + 1 < RC_PF; ++k) pf[k] = pf[k + 1];
+    pf[RC_PF - 1] = (fn + 5 + RC_PF <= fe + 4) ? p[(fn + 5 + RC_PF) * sN] : T(0);
     T Ac, Bc;
     weno5z_cell(s1v, s2v, s3, s4, s5, Ac, Bc);
     if (fn >= fs) {
@@ -512,6 +533,17 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   issue_A(fn0);
+#ifndef HGKS_HOIST_C
+#define HGKS_HOIST_C 1  // phase-C thread constants (lane roles, metrics, dt) loaded once per block, not per face
+#endif
+#if HGKS_HOIST_C
+  // lane = 16 n + 2 TT1 bl + TT1 m + a; t2 face b = BPW warp + bl
+  const int lane = threadIdx.x & 31;
+  const int a = lane % TT1, m = (lane / TT1) & 1, nn = lane >> 4;
+  const int b = (threadIdx.x >> 5) * Cfg::BPW + ((lane & 15) / (2 * TT1));
+  const T ih1 = g.jg[A1][m * n1 + min(t10 + a, n1 - 1)], ih2 = g.jg[A2][nn * n2 + min(t20 + b, n2 - 1)];
+  const T dt = T(ctl->dt), idt = T(ctl->idt);
+#endif
 #ifdef HGKS_PHASE_TIMING
   long long tA = 0, tB = 0, tC = 0;
 #endif
@@ -538,72 +570,83 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   // Item order: TT1 = 8: (a, c, l2), a half-warp reads 2 components of one row; TT1 = 4: (a, l2, c),
   // a half-warp reads 4 rows (TL1P apart) of one component -- conflict-free (TT1 = 8 except where a
   // warp straddles two rows).
-#ifndef HGKS_PB2
-#define HGKS_PB2 0  // phase B: the (up to) two items of a thread accumulated tap by tap together (ILP)
+#ifndef HGKS_PB_EO
+#define HGKS_PB_EO 0
 #endif
-#ifndef HGKS_PB2_FENCE
-#define HGKS_PB2_FENCE 1
-#endif
-  constexpr int NITEM = TT1 * 5 * TL2;
-  constexpr int NPB = HGKS_PB2 ? (NITEM + NTHREADS_FLUX - 1) / NTHREADS_FLUX : 1;
-  for (int w0 = threadIdx.x; do_ab && w0 < NITEM; w0 += NPB * NTHREADS_FLUX) {
-    T o0[NPB][NB], o1[NPB][NB];
-    const T* srcp[NPB];
-#pragma unroll
-    for (int p = 0; p < NPB; ++p) {
-      const int w = min(w0 + p * NTHREADS_FLUX, NITEM - 1);  // a thread without a second item repeats its last
-      const int a = w % TT1;
-      const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
-      const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
-      srcp[p] = sA + c * SA_C + l2 * TL1P + a;
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        o0[p][k] = T(0);
-        o1[p][k] = T(0);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
-      const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
-      if (HGKS_PB2_FENCE) asm volatile("" ::: "memory");  // loads of one tap at a time (register pressure)
-#pragma unroll
-      for (int p = 0; p < NPB; ++p) {
-#pragma unroll
-        for (int ff = 0; ff < 6; ++ff) {
-          const T x = srcp[p][ff * 5 * SA_C + r];
-          o0[p][ff] += wv0 * x;
-          o1[p][ff] += wv1 * x;
-          if (ff == 0) { o0[p][6] += wd0 * x; o1[p][6] += wd1 * x; }
-          if (ff == 1) { o0[p][7] += wd0 * x; o1[p][7] += wd1 * x; }
-          if (ff == 4) { o0[p][8] += wd0 * x; o1[p][8] += wd1 * x; }
-        }
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < NPB; ++p) {
-    const int w = w0 + p * NTHREADS_FLUX;
-    if (w >= NITEM) break;
+  // HGKS_PB_EO: the fields with a t1 derivative (Ql, Qr, C) take both abscissae from the symmetric and
+  // antisymmetric tap sums s_r = x_r + x_{4-r}, d_r = x_r - x_{4-r} (r = 0, 1):
+  //   value  E = sum (w_r + w_{4-r})/2 x_r,  O = sum (w_r - w_{4-r})/2 x_r:     v_0 = E + O, v_1 = E - O
+  //   deriv. M = sum (wd_r + wd_{4-r})/2 x_r, P = sum (wd_r - wd_{4-r})/2 x_r:   g_0 = P + M, g_1 = P - M
+  // 18 instead of 20 FP64 operations per field (the value-only fields keep the 10 direct FMAs)
+  for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
     const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
     const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
-    const T (&o0p)[NB] = o0[p];
-    const T (&o1p)[NB] = o1[p];
+    T o0[NB], o1[NB];
+    const T* src = sA + c * SA_C + l2 * TL1P + a;
+    if (HGKS_PB_EO) {
+#pragma unroll
+      for (int ff = 0; ff < 6; ++ff) {
+        T x[5];
+#pragma unroll
+        for (int r = 0; r < 5; ++r) x[r] = src[ff * 5 * SA_C + r];
+        const int kd = ff == 0 ? 6 : (ff == 1 ? 7 : (ff == 4 ? 8 : -1));  // t1-derivative slot
+        if (kd < 0) {
+          T v0 = T(0), v1 = T(0);
+#pragma unroll
+          for (int r = 0; r < 5; ++r) {
+            v0 += hgks::wv0<T>(r) * x[r];
+            v1 += hgks::wv0<T>(4 - r) * x[r];
+          }
+          o0[ff] = v0;
+          o1[ff] = v1;
+        } else {
+          const T s0 = x[0] + x[4], s1 = x[1] + x[3], d0 = x[0] - x[4], d1 = x[1] - x[3];
+          const T E = hgks::eo<T>(0) * s0 + hgks::eo<T>(1) * s1 + hgks::wv0<T>(2) * x[2];
+          const T O = hgks::eo<T>(2) * d0 + hgks::eo<T>(3) * d1;
+          const T M = hgks::eo<T>(4) * s0 + hgks::eo<T>(5) * s1 + hgks::wd0<T>(2) * x[2];
+          const T P = hgks::eo<T>(6) * d0 + hgks::eo<T>(7) * d1;
+          o0[ff] = E + O;
+          o1[ff] = E - O;
+          o0[kd] = P + M;
+          o1[kd] = P - M;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        o0[k] = T(0);
+        o1[k] = T(0);
+      }
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
+        const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
+#pragma unroll
+        for (int ff = 0; ff < 6; ++ff) {
+          const T x = src[ff * 5 * SA_C + r];
+          o0[ff] += wv0 * x;
+          o1[ff] += wv1 * x;
+          if (ff == 0) { o0[6] += wd0 * x; o1[6] += wd1 * x; }
+          if (ff == 1) { o0[7] += wd0 * x; o1[7] += wd1 * x; }
+          if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
+        }
+      }
+    }
     T* dst = sB + l2 * RS + (Cfg::VEC ? 0 : c * CS + Cfg::MA(0, a));
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       if constexpr (Cfg::VEC) {
-        dst[k * KS + Cfg::VOFF(c, Cfg::MA(0, a))] = o0p[k];
-        dst[k * KS + Cfg::VOFF(c, Cfg::MA(1, a))] = o1p[k];
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(0, a))] = o0[k];
+        dst[k * KS + Cfg::VOFF(c, Cfg::MA(1, a))] = o1[k];
       } else if constexpr (TT1 == 4 && sizeof(T) == 8) {  // (m = 0, m = 1) adjacent: one 16-byte store
-        *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0p[k], (double)o1p[k]);
+        *reinterpret_cast<double2*>(dst + k * KS) = make_double2((double)o0[k], (double)o1[k]);
       } else if constexpr (TT1 == 4) {
-        *reinterpret_cast<float2*>(dst + k * KS) = make_float2((float)o0p[k], (float)o1p[k]);
+        *reinterpret_cast<float2*>(dst + k * KS) = make_float2((float)o0[k], (float)o1[k]);
       } else {
-        dst[k * KS] = o0p[k];
-        dst[k * KS + Cfg::MA(1, 0)] = o1p[k];
+        dst[k * KS] = o0[k];
+        dst[k * KS + Cfg::MA(1, 0)] = o1[k];
       }
-    }
     }
   }
   if (do_ab) {
@@ -616,10 +659,12 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
 
   // ---- phase C: one thread per Gauss point ----------------------------------------------------
   // lane = 16 n + 2 TT1 bl + TT1 m + a; t2 face b = BPW warp + bl
+#if !HGKS_HOIST_C
   const int lane = threadIdx.x & 31;
   const int a = lane % TT1, m = (lane / TT1) & 1, nn = lane >> 4;
   const int b = (threadIdx.x >> 5) * Cfg::BPW + ((lane & 15) / (2 * TT1));
   const T ih1 = g.jg[A1][m * n1 + min(t10 + a, n1 - 1)], ih2 = g.jg[A2][nn * n2 + min(t20 + b, n2 - 1)];
+#endif
   const T sgn = nn ? T(-1) : T(1);
   // t2 pass of slot k, component c, over rows b..b+4: value (wv) or derivative (wd) at this Gauss
   // point.  n = 1 uses the mirrored weights wv[1][r] = wv[0][4-r], wd[1][r] = -wd[0][4-r]:
@@ -671,7 +716,9 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
     for (int r = 0; r < 5; ++r) v += (kRowMirror ? wd0<T>(r) : wdl[r]) * row0[r * rstep + c * CS + k * KS];
     return v;
   };
-  const T dt = T(ctl->dt);
+#if !HGKS_HOIST_C
+  const T dt = T(ctl->dt), idt = T(ctl->idt);
+#endif
   constexpr bool PRF = VAR & 1;
   GpFlux<T, STAGE == 1, PRF, (VAR >> 1) & 1> gf;
   // value and t2-derivative of Ql, Qr from the same five row loads (the t2 derivatives are held
@@ -723,7 +770,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
       T Wl[5], Wr[5];
       pass5vd(0, Wl, d2l);
       pass5vd(1, Wr, d2r);
-      gf.begin(gas, Wl, Wr, dt, T(ctl->idt));
+      gf.begin(gas, Wl, Wr, dt, idt);
     }
     gf.template add_side<+1>([&](int i, T (&d)[5]) {
       if (i == 0) pass5(2, wvl, d);
@@ -748,7 +795,7 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
       tvd(c, 0, Wl[c], d2l[c]);
       tvd(c, 1, Wr[c], d2r[c]);
     }
-    gf.begin(gas, Wl, Wr, dt, T(ctl->idt));
+    gf.begin(gas, Wl, Wr, dt, idt);
   }
   gf.template add_side<+1>([&](int i, T (&d)[5]) {
 #pragma unroll
