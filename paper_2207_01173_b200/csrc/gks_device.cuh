@@ -370,26 +370,6 @@ __device__ __forceinline__ double wv0<double>(int r) { return c_wv0[r]; }
 template <>
 __device__ __forceinline__ double wd0<double>(int r) { return c_wd0[r]; }
 #endif
-// Symmetric / antisymmetric parts of the tangential weights (phase B of the flux kernel, HGKS_PB_EO),
-// exact: w_r = kWV0(r), wd_r = kWD0(r); index 0..7 = (w0+w4)/2, (w1+w3)/2, (w0-w4)/2, (w1-w3)/2,
-// (wd0+wd4)/2, (wd1+wd3)/2, (wd0-wd4)/2, (wd1-wd3)/2
-__host__ __device__ constexpr double kEO(int i) {
-  return i == 0 ? -1.0 / 4320.0
-       : i == 1 ? 1.0 / 1080.0
-       : i == 2 ? -7.0 * HGKS_S3 / 432.0
-       : i == 3 ? 25.0 * HGKS_S3 / 216.0
-       : i == 4 ? HGKS_S3 / 54.0
-       : i == 5 ? -13.0 * HGKS_S3 / 54.0
-       : i == 6 ? 1.0 / 12.0
-                : -2.0 / 3.0;
-}
-#ifdef __CUDACC__
-__constant__ double c_eo[8] = {kEO(0), kEO(1), kEO(2), kEO(3), kEO(4), kEO(5), kEO(6), kEO(7)};
-template <class T>
-__device__ __forceinline__ T eo(int i) { return T(kEO(i)); }
-template <>
-__device__ __forceinline__ double eo<double>(int i) { return c_eo[i]; }
-#endif
 
 // ---------------------------------------------------------------------------------------------
 // Kinetic part (A4-A6).  Every Maxwellian is handled in a frame moving with it, where its

@@ -570,67 +570,29 @@ __global__ void __launch_bounds__(FluxCfg<T>::NT, FluxCfg<T>::MINB)
   // Item order: TT1 = 8: (a, c, l2), a half-warp reads 2 components of one row; TT1 = 4: (a, l2, c),
   // a half-warp reads 4 rows (TL1P apart) of one component -- conflict-free (TT1 = 8 except where a
   // warp straddles two rows).
-#ifndef HGKS_PB_EO
-#define HGKS_PB_EO 0
-#endif
-  // HGKS_PB_EO: the fields with a t1 derivative (Ql, Qr, C) take both abscissae from the symmetric and
-  // antisymmetric tap sums s_r = x_r + x_{4-r}, d_r = x_r - x_{4-r} (r = 0, 1):
-  //   value  E = sum (w_r + w_{4-r})/2 x_r,  O = sum (w_r - w_{4-r})/2 x_r:     v_0 = E + O, v_1 = E - O
-  //   deriv. M = sum (wd_r + wd_{4-r})/2 x_r, P = sum (wd_r - wd_{4-r})/2 x_r:   g_0 = P + M, g_1 = P - M
-  // 18 instead of 20 FP64 operations per field (the value-only fields keep the 10 direct FMAs)
   for (int w = threadIdx.x; do_ab && w < TT1 * 5 * TL2; w += NTHREADS_FLUX) {
     const int a = w % TT1;
     const int c = TT1 == 8 ? (w / TT1) % 5 : w / (TT1 * TL2);
     const int l2 = TT1 == 8 ? w / (TT1 * 5) : (w / TT1) % TL2;
     T o0[NB], o1[NB];
     const T* src = sA + c * SA_C + l2 * TL1P + a;
-    if (HGKS_PB_EO) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      o0[k] = T(0);
+      o1[k] = T(0);
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
+      const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
 #pragma unroll
       for (int ff = 0; ff < 6; ++ff) {
-        T x[5];
-#pragma unroll
-        for (int r = 0; r < 5; ++r) x[r] = src[ff * 5 * SA_C + r];
-        const int kd = ff == 0 ? 6 : (ff == 1 ? 7 : (ff == 4 ? 8 : -1));  // t1-derivative slot
-        if (kd < 0) {
-          T v0 = T(0), v1 = T(0);
-#pragma unroll
-          for (int r = 0; r < 5; ++r) {
-            v0 += hgks::wv0<T>(r) * x[r];
-            v1 += hgks::wv0<T>(4 - r) * x[r];
-          }
-          o0[ff] = v0;
-          o1[ff] = v1;
-        } else {
-          const T s0 = x[0] + x[4], s1 = x[1] + x[3], d0 = x[0] - x[4], d1 = x[1] - x[3];
-          const T E = hgks::eo<T>(0) * s0 + hgks::eo<T>(1) * s1 + hgks::wv0<T>(2) * x[2];
-          const T O = hgks::eo<T>(2) * d0 + hgks::eo<T>(3) * d1;
-          const T M = hgks::eo<T>(4) * s0 + hgks::eo<T>(5) * s1 + hgks::wd0<T>(2) * x[2];
-          const T P = hgks::eo<T>(6) * d0 + hgks::eo<T>(7) * d1;
-          o0[ff] = E + O;
-          o1[ff] = E - O;
-          o0[kd] = P + M;
-          o1[kd] = P - M;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        o0[k] = T(0);
-        o1[k] = T(0);
-      }
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        const T wv0 = hgks::wv0<T>(r), wd0 = hgks::wd0<T>(r);          // m = 0 weights of tap r
-        const T wv1 = hgks::wv0<T>(4 - r), wd1 = -hgks::wd0<T>(4 - r);  // m = 1 weights of tap r
-#pragma unroll
-        for (int ff = 0; ff < 6; ++ff) {
-          const T x = src[ff * 5 * SA_C + r];
-          o0[ff] += wv0 * x;
-          o1[ff] += wv1 * x;
-          if (ff == 0) { o0[6] += wd0 * x; o1[6] += wd1 * x; }
-          if (ff == 1) { o0[7] += wd0 * x; o1[7] += wd1 * x; }
-          if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
-        }
+        const T x = src[ff * 5 * SA_C + r];
+        o0[ff] += wv0 * x;
+        o1[ff] += wv1 * x;
+        if (ff == 0) { o0[6] += wd0 * x; o1[6] += wd1 * x; }
+        if (ff == 1) { o0[7] += wd0 * x; o1[7] += wd1 * x; }
+        if (ff == 4) { o0[8] += wd0 * x; o1[8] += wd1 * x; }
       }
     }
     T* dst = sB + l2 * RS + (Cfg::VEC ? 0 : c * CS + Cfg::MA(0, a));
