@@ -1,1 +1,1 @@
-bash tools/gpu_ab2.sh "" default f4 default f4
+bash tools/gpu_ab2.sh "" default rm8 rm10 default rm8
